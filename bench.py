@@ -1,0 +1,453 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 grid-generation hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): per GPU, 1024 synthetic molecules of
+the config-0 distribution -> fp32 grids [1024, 5, 64, 64, 64] over a 12 A
+cube, sigma 0.5 (5.37 GB of output per step, 42x the 126 MB L2, so every
+step streams to HBM; the atom inputs are tiny and stay resident).
+
+A *step* = one pass of the hot path over the batch: K1 (per-atom axis
+tables) + K3 (slab gather/store, all voxels incl. zeros, fused nonzero
+counters). ``value`` = grids/s over all ranks (inputs resident in HBM);
+``e2e`` = the same metric through the public API ``generate_packed`` with
+host (pinned) CSR inputs copied H2D and the per-grid stats read back D2H
+inside the timed region. ``roofline`` = K3's algorithmic bytes (the output)
+per launch / its CUDA-event duration vs the measured HBM peak.
+
+Multi-GPU: one process per GPU (torchrun), molecules sharded by rank with no
+collective on the data path (weak scaling: every rank generates its own
+1024-molecule batch); NCCL is used only for the barrier and the max-over-
+ranks time. ``--impl reference`` times the reference's CPU algorithm (the
+numpy oracle port, oracle/) on this host's cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--config", type=int, default=1, help="BASELINE config index (default 1)")
+    ap.add_argument("--batch", type=int, default=None, help="molecules per GPU (default: config)")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:  # noqa: BLE001
+            pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML polling thread)
+# ---------------------------------------------------------------------------
+_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._thread = None
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # noqa: BLE001
+            log(f"[bench] NVML unavailable for clock sampling: {exc}")
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        names = [n for bit, n in _REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (barrier + max over ranks only)
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    def __init__(self, world, rank, local):
+        import torch
+
+        self.world, self.rank, self.local = world, rank, local
+        self.torch = torch
+        self.pg = None
+        if world > 1:
+            import torch.distributed as td
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.td = td
+            self.pg = True
+
+    def barrier(self):
+        if self.pg:
+            self.td.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if not self.pg:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.td.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference algorithm (oracle port) on this host's cores
+# ---------------------------------------------------------------------------
+def cpu_rate(cfg, seconds: float, workers: int):
+    """grids/s of the oracle port over a bounded sample of ``cfg``."""
+    from oracle import voxgrid_oracle as orc
+    from paper_2211_08506_b200 import synth
+
+    geom = orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents, cfg.sigma)
+    probe = synth.packed_batch(cfg, range(8))
+    t0 = time.perf_counter()
+    orc.batch(probe.offsets, probe.channels, probe.xyz, geom, workers=1)
+    per_grid = (time.perf_counter() - t0) / 8
+    n = int(min(cfg.n_molecules * 4, max(workers * 4, seconds * workers / max(per_grid, 1e-6))))
+    pb = synth.packed_batch(cfg, range(n))
+    t0 = time.perf_counter()
+    orc.batch(pb.offsets, pb.channels, pb.xyz, geom, workers=workers)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import voxgrid_oracle as orc
+    from paper_2211_08506_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    workers = orc.host_cores()
+    geom = orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents, cfg.sigma)
+    # bounded per-step sample: ~2-3 s of work on all cores
+    probe = synth.packed_batch(cfg, range(8))
+    t0 = time.perf_counter()
+    orc.batch(probe.offsets, probe.channels, probe.xyz, geom, workers=1)
+    per_grid = (time.perf_counter() - t0) / 8
+    n = int(max(workers * 2, min(cfg.n_molecules, 2.5 * workers / max(per_grid, 1e-6))))
+    pb = synth.packed_batch(cfg, range(n))
+    from concurrent.futures import ProcessPoolExecutor
+
+    jobs = [(pb.channels[pb.offsets[b]:pb.offsets[b + 1]], pb.xyz[pb.offsets[b]:pb.offsets[b + 1]],
+             geom, "sparse", None) for b in range(n)]
+    chunk = max(1, n // (workers * 4))
+    with ProcessPoolExecutor(max_workers=workers) as pool:
+        for _ in range(args.warmup):
+            list(pool.map(orc._one, jobs, chunksize=chunk))
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            list(pool.map(orc._one, jobs, chunksize=chunk))
+        dt = time.perf_counter() - t0
+    rate = n * args.steps / dt
+    H, W, D = cfg.shape
+    sample = (f"{n} molecules of {cfg.name} per step (numpy port of voxgrid.generate_grid, "
+              f"process pool of {workers})")
+    line = {
+        "impl": "reference", "metric": "grids_per_sec", "value": rate, "unit": "grids/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "voxels_per_sec": rate * cfg.channels * H * W * D,
+        "config": {"workload": f"{cfg.name}: CPU sample of {n} molecules per step",
+                   "grid": [cfg.channels, H, W, D], "sigma": cfg.sigma},
+        "cpu_baseline": {"value": rate, "unit": "grids/s", "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "grids/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = Dist(world, rank, local)
+    import paper_2211_08506_b200 as vg
+    from paper_2211_08506_b200 import _native, shard, synth
+
+    cfg = synth.CONFIGS[args.config]
+    B = args.batch or cfg.n_molecules
+    if args.scaling == "weak":
+        indices = range(rank * B, (rank + 1) * B)       # distinct molecules per rank
+    else:
+        indices = shard.shard_range(B, rank, world)       # fixed total, split by rank
+    t0 = time.perf_counter()
+    pb = synth.packed_batch(cfg, indices)
+    log(f"[bench rank{rank}] synthesized {pb.n_molecules} molecules / {len(pb.channels)} atoms "
+        f"in {time.perf_counter() - t0:.1f}s")
+    Bl = pb.n_molecules
+    H, W, D = cfg.shape
+    spec = vg.GridSpec(cfg.shape, cfg.channels, vg.BoundingBox(cfg.box_origin, cfg.box_extents),
+                       cfg.sigma)
+    dev = torch.device("cuda", local)
+    eng = vg.GridEngine(dev)
+    lib = _native.lib()
+    stream = torch.cuda.current_stream(dev)
+
+    # device-resident inputs for the `value` leg
+    off_d = torch.from_numpy(pb.offsets).to(dev)
+    ch_d = torch.from_numpy(pb.channels).to(dev)
+    xyz_d = torch.from_numpy(pb.xyz).to(dev)
+    out = torch.empty((Bl, cfg.channels, H, W, D), dtype=torch.float32, device=dev)
+    stats = torch.empty((Bl, 2), dtype=torch.int64, device=dev)
+    desc = eng.describe(off_d, ch_d, xyz_d, spec)
+    layout = _native.VgWsLayout()
+    _native.check(lib.vg_workspace_layout(desc, layout), "layout")
+    ws = torch.empty(layout.total, dtype=torch.uint8, device=dev)
+    sptr = stream.cuda_stream
+
+    def step():
+        _native.check(lib.vg_axis_tables_f32(desc, ws.data_ptr(), ws.numel(), sptr), "tables")
+        _native.check(lib.vg_slabs_f32(desc, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       stats.data_ptr(), sptr), "slabs")
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    sampler = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for k in range(K):
+            ev[k][0].record(stream)
+            _native.check(lib.vg_axis_tables_f32(desc, ws.data_ptr(), ws.numel(), sptr), "tables")
+            ev[k][1].record(stream)
+            _native.check(lib.vg_slabs_f32(desc, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                           stats.data_ptr(), sptr), "slabs")
+            ev[k][2].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    total_ms = ev[0][0].elapsed_time(ev[-1][2])
+    k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    k3_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    t_max = dist.max(total_ms)
+    grids_total = dist.sum(float(Bl)) * K
+    value = grids_total / (t_max / 1e3)
+    launches = 2 * K
+
+    # roofline of K3 (dominant kernel): algorithmic bytes = the output grids
+    alg_bytes = Bl * cfg.grid_bytes
+    k3_avg = statistics.mean(k3_ms)
+    achieved = alg_bytes / (k3_avg / 1e3) / 1e9
+    peak, peak_src = peaks()
+
+    # pure-write fill of the same bytes: what HBM sustains for stores alone
+    for _ in range(3):
+        _native.check(lib.vg_fill_f32(out.data_ptr(), out.numel(), 0.0, sptr), "fill")
+    fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fa.record(stream)
+    for _ in range(5):
+        _native.check(lib.vg_fill_f32(out.data_ptr(), out.numel(), 0.0, sptr), "fill")
+    fb.record(stream)
+    torch.cuda.synchronize()
+    fill_gbs = alg_bytes * 5 / (fa.elapsed_time(fb) / 1e3) / 1e9
+
+    # e2e through the public API: pinned host CSR -> H2D -> kernels -> D2H stats
+    off_h = torch.from_numpy(pb.offsets).pin_memory()
+    ch_h = torch.from_numpy(pb.channels).pin_memory()
+    xyz_h = torch.from_numpy(pb.xyz).pin_memory()
+    st_h = torch.empty((Bl, 2), dtype=torch.int64).pin_memory()
+    h2d = off_h.numel() * 8 + ch_h.numel() * 4 + xyz_h.numel() * 8
+    d2h = st_h.numel() * 8
+
+    def e2e_step():
+        _, st = vg.generate_packed(off_h, ch_h, xyz_h, spec, out=out, engine=eng)
+        st_h.copy_(st, non_blocking=True)
+
+    for _ in range(max(args.warmup, 3)):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    ea.record(stream)
+    for _ in range(K):
+        e2e_step()
+    eb.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    e2e_ms = max(ea.elapsed_time(eb), wall * 1e3)
+    e2e_value = grids_total / (dist.max(e2e_ms) / 1e3)
+    dist.barrier()
+
+    line = None
+    if rank == 0:
+        n_atoms = len(pb.channels)
+        line = {
+            "metric": "grids_per_sec",
+            "value": value,
+            "unit": "grids/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": t_max / K,
+            "higher_is_better": True,
+            "scaling": args.scaling,
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (seeded BASELINE config distribution; no dataset)",
+            "voxels_per_sec": value * cfg.channels * H * W * D,
+            "config": {
+                "workload": f"{cfg.name}: {Bl} molecules/GPU -> fp32 "
+                            f"[{Bl},{cfg.channels},{H},{W},{D}], sigma {cfg.sigma}, "
+                            f"box {cfg.box_extents[0]} A",
+                "global_batch": int(grids_total / K),
+                "grid": [cfg.channels, H, W, D],
+                "atoms_per_gpu": n_atoms,
+                "parallelism": f"molecule-sharded x{world}, no collective",
+                "l2": "no flush needed: each step writes "
+                      f"{alg_bytes / 1e9:.2f} GB >> 126 MB L2",
+            },
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "vg_slab_kernel (K3)",
+                "achieved": achieved,
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": traffic_from_profiles(args.config),
+                "alg_bytes_per_launch": alg_bytes,
+                "k3_ms": k3_avg,
+                "k1_ms": statistics.mean(k1_ms),
+                "k3_share_of_step": k3_avg / (total_ms / K),
+                "write_fill_gbs": fill_gbs,
+            },
+            "e2e": {"value": e2e_value, "unit": "grids/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "api": "paper_2211_08506_b200.generate_packed(pinned host CSR)"},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+    dist.close()
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import voxgrid_oracle as orc
+
+            workers = orc.host_cores()
+            rate, n, dt = cpu_rate(cfg, args.cpu_seconds, workers)
+            line["cpu_baseline"] = {
+                "value": rate, "unit": "grids/s", "cores": workers, "kind": "port",
+                "sample": f"{n} molecules of {cfg.name} in {dt:.1f}s (numpy port of "
+                          f"voxgrid.generate_grid, process pool)"}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def traffic_from_profiles(config: int):
+    """dram bytes per K3 launch from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(f"cfg{config}")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

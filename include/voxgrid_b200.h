@@ -1,0 +1,117 @@
+/* voxgrid_b200.h — C-ABI of the B200 grid-generation hot path.
+ *
+ * Drop-in boundary for the reference package `voxgrid` (pure Python/numpy,
+ * /root/reference/pkg/src/voxgrid). Each entry point names the reference
+ * interface it replaces. Plain pointers and sizes only: device pointers are
+ * CUDA global-memory addresses, `stream` is a cudaStream_t passed as void*.
+ * The library never allocates or frees device memory and keeps no global
+ * state besides a thread-local error string; every launch is stream-ordered
+ * with no host synchronisation, so calls are reentrant across streams.
+ *
+ * Return codes: VG_OK (0) or a negative VG_ERR_*; vg_last_error() explains.
+ */
+#ifndef VOXGRID_B200_H
+#define VOXGRID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VG_OK 0
+#define VG_ERR_INVALID -1   /* bad descriptor / argument (ValueError in Python) */
+#define VG_ERR_CUDA -2      /* a CUDA launch or runtime call failed             */
+#define VG_ERR_WORKSPACE -3 /* workspace pointer NULL or too small              */
+
+#define VG_ABI_VERSION 1
+
+/* One batch of molecules in CSR form plus the grid geometry.
+ *
+ * Geometry follows GridSpec (reference core.py:92-166): shape (H, W, D) =
+ * voxels along (y, x, z); axis_params() gives per world axis x,y,z the triple
+ * (n, origin, delta) = (W, ox, A/W), (H, oy, B/H), (D, oz, C/D)
+ * (core.py:161-166). Output layout is (B, C, H, W, D) fp32, z contiguous
+ * (core.py:3-19); voxel (i, j, k) of channel c is out[b, c, j, i, k].
+ */
+typedef struct vg_batch_desc {
+  int64_t n_molecules;       /* B                                               */
+  int64_t n_atoms;           /* total atoms over the batch                      */
+  const int64_t* offsets;    /* device [B+1]; molecule b owns atoms [o[b],o[b+1]) */
+  const double* xyz;         /* device [n_atoms*3] world positions (x,y,z), fp64 */
+  const int32_t* channel;    /* device [n_atoms] channel in [0, C)              */
+  const double* mol_origin;  /* device [B*3] per-molecule box origin, or NULL   */
+  const double* mol_delta;   /* device [B*3] per-molecule voxel sizes, or NULL  */
+  double origin[3];          /* shared box origin (x,y,z) when mol_origin==NULL */
+  double delta[3];           /* shared voxel sizes (dx,dy,dz) when mol_delta==NULL */
+  double scale;              /* 1/(sigma*sqrt(2)) in fp64, kernels.py:235        */
+  float threshold;           /* fl32(threshold), or NaN for None (kernels.py:271) */
+  int32_t periodic;          /* 1: wrap every axis, cell edge = n*delta (kernels.py:239-251) */
+  int32_t H, W, D, C;        /* grid shape (y, x, z) and channel count          */
+} vg_batch_desc;
+
+/* Per-molecule work counters, GenStats (gridgen.py:39-54) minus the
+ * host-side fields. voxel_writes = sum over atoms of the support-box volume
+ * (gridgen.py:103); nonzero_voxels = count_nonzero of the grid (gridgen.py:151). */
+typedef struct vg_mol_stats {
+  int64_t voxel_writes;
+  int64_t nonzero_voxels;
+} vg_mol_stats;
+
+/* Byte offsets of the per-atom tables inside the workspace (all 256-aligned).
+ * tx: [n_atoms][row_x] fp32 masses along x (W used), ty: [n_atoms][row_y] (H),
+ * tz: [n_atoms][row_z] (D); supp: [n_atoms] x int32[4] =
+ * {xlo | xhi<<16, ylo | yhi<<16, zlo | zhi<<16, channel} (AxisTable.support,
+ * kernels.py:101-119, 147-151). */
+typedef struct vg_ws_layout {
+  size_t tx, ty, tz, supp, total;
+  int32_t row_x, row_y, row_z;
+} vg_ws_layout;
+
+/* Workspace needed by vg_generate_f32 / vg_axis_tables_f32. */
+int vg_workspace_layout(const vg_batch_desc* desc, vg_ws_layout* layout);
+
+/* Replaces generate_batch (gridgen.py:173-221) / generate_grid
+ * (gridgen.py:130-153) for float32 grids: writes every voxel of
+ * out[B, C, H, W, D] (zeros included; no prior memset needed). Per voxel the
+ * atoms of its channel are accumulated in input order in fp32 exactly as
+ * splat_atom (gridgen.py:97-109). stats (device [B]) may be NULL. */
+int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspace,
+                    size_t workspace_bytes, vg_mol_stats* stats, void* stream);
+
+/* The second half of vg_generate_f32 alone: writes out[B, C, H, W, D] from
+ * tables already computed into `workspace` by vg_axis_tables_f32 for the same
+ * descriptor (stream-ordered). Lets a caller time the slab kernel by itself or
+ * regenerate grids from cached tables. */
+int vg_slabs_f32(const vg_batch_desc* desc, float* out, const void* workspace,
+                 size_t workspace_bytes, vg_mol_stats* stats, void* stream);
+
+/* Replaces fused_axis_tables (kernels.py:217-274) for every atom of the
+ * batch: fills the workspace tables + supports (layout above). Test hook and
+ * building block for consumers (reversal) that need the tables. */
+int vg_axis_tables_f32(const vg_batch_desc* desc, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Replaces erf_approx(t, float32) (kernels.py:59-70) on a device array. */
+int vg_erf_f32(const float* t, float* out, int64_t n, void* stream);
+
+/* Device fill with 128-bit stores (HBM write-bandwidth probe for the roofline). */
+int vg_fill_f32(float* out, int64_t n, float value, void* stream);
+
+/* Host builds of the exact device numerics, for conformance tests only:
+ * np.exp on float32 (numpy SIMD algorithm) and the Bürmann erf. */
+int vg_exp_f32_host(const float* x, float* out, size_t n);
+int vg_erf_f32_host(const float* t, float* out, size_t n);
+
+/* Thread-local description of the last error (empty string if none). */
+const char* vg_last_error(void);
+
+/* VG_ABI_VERSION of the loaded library. */
+int vg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VOXGRID_B200_H */

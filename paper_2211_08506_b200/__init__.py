@@ -1,0 +1,66 @@
+"""voxgrid-b200: B200-native batched molecule -> Gaussian-density grid generation.
+
+Drop-in for the grid-generation path of the reference package ``voxgrid``
+(ParticleGrid, arXiv 2211.08506): same names and arguments, device-resident
+float32 grids ``(B, C, H, W, D)`` computed by hand-written sm_100a kernels.
+See DESIGN.md for the boundary and INTEGRATION.md for the C-ABI.
+"""
+
+from .core import (
+    BoundingBox,
+    Grid,
+    GridSpec,
+    LatticeCell,
+    ParticleSet,
+    bounding_box_of,
+    voxel_to_world,
+    world_to_voxel,
+)
+from .gridgen import (
+    BatchResult,
+    GenStats,
+    GridEngine,
+    default_engine,
+    generate_batch,
+    generate_grid,
+    generate_packed,
+)
+from .kernels import ERF_C1, ERF_C2, AxisTable, axis_tables_batch, erf_approx, fused_axis_tables
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # deferred like the reference (__init__.py:59-65): sklearn only when asked
+    if name == "GaussianVoxelizer":
+        from .estimator import GaussianVoxelizer
+
+        return GaussianVoxelizer
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+
+
+__all__ = [
+    "BoundingBox",
+    "Grid",
+    "GridSpec",
+    "LatticeCell",
+    "ParticleSet",
+    "bounding_box_of",
+    "voxel_to_world",
+    "world_to_voxel",
+    "BatchResult",
+    "GenStats",
+    "GridEngine",
+    "default_engine",
+    "generate_batch",
+    "generate_grid",
+    "generate_packed",
+    "ERF_C1",
+    "ERF_C2",
+    "AxisTable",
+    "axis_tables_batch",
+    "erf_approx",
+    "fused_axis_tables",
+    "GaussianVoxelizer",
+    "__version__",
+]

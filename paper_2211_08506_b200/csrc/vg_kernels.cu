@@ -1,0 +1,659 @@
+// vg_kernels.cu — sm_100a kernels + C-ABI for batched Gaussian-density grids.
+//
+// Path replaced (reference /root/reference/pkg/src/voxgrid):
+//   generate_batch   gridgen.py:173-221  -> vg_generate_f32
+//   generate_grid    gridgen.py:130-153  -> vg_generate_f32 (B = 1)
+//   splat_atom       gridgen.py:74-111   -> K3 vg_slab_kernel (per-voxel gather)
+//   fused_axis_tables kernels.py:217-274 -> K1 vg_tables_kernel
+//   erf_approx       kernels.py:49-70    -> vg_math.cuh / vg_erf_kernel
+//
+// Design:
+//   K1  one warp per (atom, axis): n+1 edge erf values (shared endpoints,
+//       kernels.py:256-262), masses 0.5*dE, optional threshold, exact support
+//       [first nonzero, last nonzero+1) by warp ballots. Tables go to a global
+//       workspace that K3 reads through L1/L2.
+//   K3  one CTA per (molecule, channel, y-chunk, slot block). The CTA builds
+//       the ordered list of candidate atoms of its channel whose y-support
+//       meets the chunk (block-wide ordered compaction, no atomics), then for
+//       every y-slab writes the (W x D) slab exactly once: each thread owns a
+//       float4 of z-contiguous voxels, accumulates the candidates in input
+//       order (fl32(acc + fl32(fl32(gy*gx)*gz)), gridgen.py:105-109) and
+//       issues one coalesced 128-bit store. Warps whose rows miss an atom's
+//       x-support skip it (a skipped term is exactly +0, so culling is exact).
+//   No float atomics anywhere: output bits are independent of launch shape.
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/voxgrid_b200.h"
+#include "vg_math.cuh"
+
+#define VG_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof g_last_error, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(VG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(err));
+  return VG_OK;
+}
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
+constexpr int kListCap = 1024;       // K3: candidate segment capacity
+constexpr int kMaxThreads = 256;     // K3: threads per CTA (upper bound)
+constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+int round_up4(int v) { return (v + 3) & ~3; }
+
+// ---------------------------------------------------------------------------
+// K1: per-atom axis tables
+// ---------------------------------------------------------------------------
+struct TableParams {
+  const int64_t* offsets;
+  const double* xyz;
+  const int32_t* channel;
+  const double* mol_origin;
+  const double* mol_delta;
+  float* tbl[3];
+  int32_t* supp;
+  double origin[3];
+  double delta[3];
+  double scale;
+  int64_t n_atoms;
+  int64_t n_molecules;
+  int n[3];
+  int row[3];
+  float threshold;
+  int has_threshold;
+  int periodic;
+};
+
+// Python float `%` for a positive divisor (kernels.py:247): fmod is exact in
+// IEEE arithmetic; the result takes the divisor's sign, +0 for exact zeros.
+__device__ __forceinline__ double py_mod(double x, double y) {
+  double r = fmod(x, y);
+  if (r != 0.0) {
+    if ((y < 0.0) != (r < 0.0)) r = __dadd_rn(r, y);
+  } else {
+    r = copysign(0.0, y);
+  }
+  return r;
+}
+
+// Largest b with offsets[b] <= atom: the molecule that owns `atom` (empty
+// molecules share their offset with the next one and are skipped).
+__device__ __forceinline__ int64_t owner_of(const int64_t* offsets, int64_t n_mol, int64_t atom) {
+  int64_t lo = 0, hi = n_mol - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(offsets + mid) <= atom) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (kTableThreads / 32) + (threadIdx.x >> 5);
+  if (gw >= p.n_atoms * 3) return;
+  const int64_t atom = gw / 3;
+  const int axis = (int)(gw - atom * 3);
+  const int n = p.n[axis];
+
+  double o = p.origin[axis];
+  double d = p.delta[axis];
+  if (p.mol_origin != nullptr || p.mol_delta != nullptr) {
+    const int64_t b = owner_of(p.offsets, p.n_molecules, atom);
+    if (p.mol_origin != nullptr) o = p.mol_origin[b * 3 + axis];
+    if (p.mol_delta != nullptr) d = p.mol_delta[b * 3 + axis];
+  }
+  const double mu = p.xyz[atom * 3 + axis];
+  const double s = p.scale;
+
+  // Edge arguments are rel + delta*e (fp64) times s. Open axis: rel = o - mu
+  // (kernels.py:253). Periodic: images p in (r-L, r, r+L), rel = -p, with
+  // r = (mu - o) % L and L = n*delta (kernels.py:240, 247-251).
+  double rel[3];
+  int images = 1;
+  if (!p.periodic) {
+    rel[0] = __dsub_rn(o, mu);
+    rel[1] = rel[2] = 0.0;
+  } else {
+    const double L = __dmul_rn((double)n, d);
+    const double r = py_mod(__dsub_rn(mu, o), L);
+    rel[0] = -__dsub_rn(r, L);
+    rel[1] = -r;
+    rel[2] = -__dadd_rn(r, L);
+    images = 3;
+  }
+
+  float* tbl = p.tbl[axis] + atom * p.row[axis];
+  float e_cur[3], e_nxt[3];
+#pragma unroll
+  for (int im = 0; im < 3; ++im) {
+    e_cur[im] = 0.0f;
+    if (im < images && lane <= n) e_cur[im] = vg_erf_f32(vg_edge_arg(rel[im], d, lane, s));
+  }
+  int lo = -1, hi = 0;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int e = c0 + lane;
+    // erf at the next chunk's edges (each edge evaluated exactly once)
+#pragma unroll
+    for (int im = 0; im < 3; ++im) {
+      e_nxt[im] = 0.0f;
+      if (im < images && e + 32 <= n) e_nxt[im] = vg_erf_f32(vg_edge_arg(rel[im], d, e + 32, s));
+    }
+    float g = 0.0f;
+#pragma unroll
+    for (int im = 0; im < 3; ++im) {
+      if (im < images) {
+        float up = __shfl_down_sync(kFull, e_cur[im], 1);
+        const float wrap = __shfl_sync(kFull, e_nxt[im], 0);
+        if (lane == 31) up = wrap;
+        // half * (E[e+1] - E[e]), kernels.py:260; images summed (g-1 + g0) + g+1, :268
+        const float gi = VG_FMUL(0.5f, VG_FSUB(up, e_cur[im]));
+        g = (im == 0) ? gi : VG_FADD(g, gi);
+      }
+    }
+    if (p.has_threshold && !(g >= p.threshold)) g = 0.0f;  // kernels.py:271-272
+    if (e < n) tbl[e] = g;
+    const unsigned nz = __ballot_sync(kFull, e < n && g != 0.0f);
+    if (nz != 0u) {
+      if (lo < 0) lo = c0 + __ffs(nz) - 1;
+      hi = c0 + 32 - __clz(nz);
+    }
+#pragma unroll
+    for (int im = 0; im < 3; ++im) e_cur[im] = e_nxt[im];
+  }
+  if (lane == 0) {
+    const int slo = lo < 0 ? 0 : lo;   // _support_of: (0, 0) when all zero
+    const int shi = lo < 0 ? 0 : hi;
+    p.supp[atom * 4 + axis] = slo | (shi << 16);
+    if (axis == 0) p.supp[atom * 4 + 3] = p.channel[atom];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: slab gather + single coalesced store of every voxel
+// ---------------------------------------------------------------------------
+struct SlabParams {
+  const int64_t* offsets;
+  const float* tx;
+  const float* ty;
+  const float* tz;
+  const int4* supp;
+  float* out;
+  vg_mol_stats* stats;
+  int64_t slab_elems;   // W*D
+  int rx, ry, rz;       // table row strides
+  int H, C;
+  int jc;               // y-slabs per task
+  int n_jchunks;
+  int slot_blocks;      // CTAs per slab along the slot axis
+  int nslots;           // slots per slab (float4 or float)
+  int slots_per_row;    // D/4 (vector) or D (scalar)
+  int m_steps;          // slot steps per thread per slab
+};
+
+struct SlabShared {
+  int4 meta[kListCap + kMaxThreads];  // {x supp, y supp, z supp, atom}
+  int warp_cnt[kMaxThreads / 32];
+  long long red[kMaxThreads / 32];
+};
+
+__device__ __forceinline__ int lo16(int v) { return v & 0xffff; }
+__device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
+
+// Block-wide ordered compaction: scans atoms [pos, a1) in rounds of
+// blockDim.x and appends, in ascending atom order, every atom of channel c
+// with a non-empty support box whose y-support meets [jlo, jhi). Stops once
+// at least kListCap entries are held; `pos` returns the resume point.
+__device__ int build_list(const SlabParams& p, SlabShared& sh, int64_t& pos, int64_t a1, int c,
+                          int jlo, int jhi) {
+  const int nt = blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
+  int count = 0;
+  while (pos < a1 && count < kListCap) {
+    const int64_t idx = pos + threadIdx.x;
+    bool keep = false;
+    int4 s = make_int4(0, 0, 0, 0);
+    if (idx < a1) {
+      s = __ldg(p.supp + idx);
+      keep = s.w == c && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
+             hi16(s.y) > jlo;
+    }
+    const unsigned bal = __ballot_sync(kFull, keep);
+    if (lane == 0) sh.warp_cnt[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nw; ++w) {
+      const int v = sh.warp_cnt[w];
+      before += (w < warp) ? v : 0;
+      total += v;
+    }
+    if (keep) {
+      const int rank = before + __popc(bal & ((1u << lane) - 1u));
+      sh.meta[count + rank] = make_int4(s.x, s.y, s.z, (int)idx);
+    }
+    count += total;
+    pos += nt;
+    __syncthreads();
+  }
+  return count;
+}
+
+template <bool VEC>
+struct SlotT;
+template <>
+struct SlotT<true> { using T = float4; };
+template <>
+struct SlotT<false> { using T = float; };
+
+__device__ __forceinline__ void zero_slot(float4& a) { a = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void zero_slot(float& a) { a = 0.f; }
+__device__ __forceinline__ int nonzeros(const float4& a) {
+  return (a.x != 0.f) + (a.y != 0.f) + (a.z != 0.f) + (a.w != 0.f);
+}
+__device__ __forceinline__ int nonzeros(const float& a) { return a != 0.f; }
+
+// acc += fl32(pyx * gz) elementwise, never contracted to FMA.
+__device__ __forceinline__ void add_terms(float4& acc, float pyx, const float* gzrow, int k) {
+  const float4 gz = __ldg(reinterpret_cast<const float4*>(gzrow) + k);
+  acc.x = VG_FADD(acc.x, VG_FMUL(pyx, gz.x));
+  acc.y = VG_FADD(acc.y, VG_FMUL(pyx, gz.y));
+  acc.z = VG_FADD(acc.z, VG_FMUL(pyx, gz.z));
+  acc.w = VG_FADD(acc.w, VG_FMUL(pyx, gz.w));
+}
+__device__ __forceinline__ void add_terms(float& acc, float pyx, const float* gzrow, int k) {
+  acc = VG_FADD(acc, VG_FMUL(pyx, __ldg(gzrow + k)));
+}
+
+// Accumulates candidates meta[0..n) (ascending atom order) into one slot.
+template <bool VEC>
+__device__ __forceinline__ void gather_slot(const SlabParams& p, const int4* meta, int n, int j,
+                                            bool valid, int i, int k,
+                                            typename SlotT<VEC>::T& acc) {
+  for (int q = 0; q < n; ++q) {
+    const int4 s = meta[q];
+    if (j < lo16(s.y) || j >= hi16(s.y)) continue;  // uniform: y-support
+    const bool hit = valid && i >= lo16(s.x) && i < hi16(s.x);
+    if (!__any_sync(kFull, hit)) continue;           // uniform: warp rows miss x-support
+    if (valid) {
+      const int64_t a = s.w;
+      const float gy = __ldg(p.ty + a * p.ry + j);
+      const float pyx = VG_FMUL(gy, __ldg(p.tx + a * p.rx + i));  // multiply.outer(ty, tx)
+      add_terms(acc, pyx, p.tz + a * p.rz, k);                     // (.. ) outer tz, then +=
+    }
+  }
+}
+
+__device__ __forceinline__ void store_slot(float* slab, int f, const float4& v) {
+  reinterpret_cast<float4*>(slab)[f] = v;
+}
+__device__ __forceinline__ void store_slot(float* slab, int f, const float& v) { slab[f] = v; }
+
+__device__ long long block_sum(SlabShared& sh, long long v) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh.red[warp] = v;
+  __syncthreads();
+  long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nw; ++w) t += sh.red[w];
+  return t;  // valid in thread 0
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kMaxThreads) vg_slab_kernel(SlabParams p) {
+  using Slot = typename SlotT<VEC>::T;
+  __shared__ SlabShared sh;
+  const int nt = blockDim.x;
+
+  int64_t t = blockIdx.x;
+  const int sb = (int)(t % p.slot_blocks);
+  t /= p.slot_blocks;
+  const int chunk = (int)(t % p.n_jchunks);
+  t /= p.n_jchunks;
+  const int c = (int)(t % p.C);
+  const int64_t b = t / p.C;
+
+  const int64_t a0 = __ldg(p.offsets + b), a1 = __ldg(p.offsets + b + 1);
+  const int j0 = chunk * p.jc;
+  const int j1 = min(p.H, j0 + p.jc);
+  const int slot0 = sb * nt * p.m_steps;
+
+  int64_t pos = a0;
+  const int n_list = build_list(p, sh, pos, a1, c, j0, j1);
+  const bool single = pos >= a1;  // every candidate of the chunk fits the list
+
+  float* out_c = p.out + ((b * p.C + c) * (int64_t)p.H) * p.slab_elems;
+  long long nz = 0;
+  for (int j = j0; j < j1; ++j) {
+    float* slab = out_c + (int64_t)j * p.slab_elems;
+    for (int m = 0; m < p.m_steps; ++m) {
+      const int f = slot0 + m * nt + (int)threadIdx.x;
+      const bool valid = f < p.nslots;
+      const int i = f / p.slots_per_row;
+      const int k = f - i * p.slots_per_row;
+      Slot acc;
+      zero_slot(acc);
+      if (single) {
+        gather_slot<VEC>(p, sh.meta, n_list, j, valid, i, k, acc);
+      } else {
+        // Overflow path (chunks with > kListCap candidates): rebuild the
+        // slab's list segment by segment; order across segments is ascending.
+        int64_t pos2 = a0;
+        while (pos2 < a1) {
+          __syncthreads();
+          const int n2 = build_list(p, sh, pos2, a1, c, j, j + 1);
+          gather_slot<VEC>(p, sh.meta, n2, j, valid, i, k, acc);
+        }
+        __syncthreads();
+      }
+      if (valid) {
+        store_slot(slab, f, acc);
+        if (p.stats != nullptr) nz += nonzeros(acc);
+      }
+    }
+  }
+
+  if (p.stats != nullptr) {
+    const long long tot = block_sum(sh, nz);
+    if (threadIdx.x == 0 && tot != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[b].nonzero_voxels),
+                (unsigned long long)tot);
+    if (c == 0 && chunk == 0 && sb == 0) {
+      // voxel_writes = sum of support-box volumes (gridgen.py:103)
+      long long w = 0;
+      for (int64_t a = a0 + threadIdx.x; a < a1; a += nt) {
+        const int4 s = __ldg(p.supp + a);
+        w += (long long)(hi16(s.x) - lo16(s.x)) * (hi16(s.y) - lo16(s.y)) * (hi16(s.z) - lo16(s.z));
+      }
+      const long long wt = block_sum(sh, w);
+      if (threadIdx.x == 0) p.stats[b].voxel_writes = wt;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers
+// ---------------------------------------------------------------------------
+__global__ void vg_erf_kernel(const float* __restrict__ t, float* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = vg_erf_f32(t[i]);
+}
+
+__global__ void vg_fill_kernel(float4* __restrict__ out, int64_t n4, float4 v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+__global__ void vg_fill_tail_kernel(float* __restrict__ out, int64_t n, float v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// host-side validation + launch planning
+// ---------------------------------------------------------------------------
+int validate(const vg_batch_desc* d) {
+  if (d == nullptr) return set_error(VG_ERR_INVALID, "descriptor is NULL");
+  if (d->n_molecules < 0 || d->n_atoms < 0)
+    return set_error(VG_ERR_INVALID, "negative molecule or atom count");
+  if (d->n_atoms >= (int64_t)INT_MAX)
+    return set_error(VG_ERR_INVALID, "n_atoms %lld exceeds 2^31-1", (long long)d->n_atoms);
+  if (d->H < 1 || d->W < 1 || d->D < 1 || d->H > kMaxAxis || d->W > kMaxAxis || d->D > kMaxAxis)
+    return set_error(VG_ERR_INVALID, "shape (%d, %d, %d) must be 3 voxel counts in [1, %d]", d->H,
+                     d->W, d->D, kMaxAxis);
+  if (d->C < 1) return set_error(VG_ERR_INVALID, "channels must be >= 1, got %d", d->C);
+  if (!(d->scale > 0.0) || !std::isfinite(d->scale))
+    return set_error(VG_ERR_INVALID, "scale 1/(sigma*sqrt(2)) must be positive and finite");
+  if (d->n_molecules > 0 && d->offsets == nullptr)
+    return set_error(VG_ERR_INVALID, "offsets is NULL");
+  if (d->n_atoms > 0 && (d->xyz == nullptr || d->channel == nullptr))
+    return set_error(VG_ERR_INVALID, "xyz/channel is NULL with n_atoms > 0");
+  for (int a = 0; a < 3; ++a) {
+    if (d->mol_delta == nullptr && !(d->delta[a] > 0.0))
+      return set_error(VG_ERR_INVALID, "voxel size must be positive, got %g", d->delta[a]);
+  }
+  return VG_OK;
+}
+
+void fill_layout(const vg_batch_desc* d, vg_ws_layout* L) {
+  const size_t na = (size_t)d->n_atoms;
+  L->row_x = round_up4(d->W);
+  L->row_y = round_up4(d->H);
+  L->row_z = round_up4(d->D);
+  size_t off = 0;
+  L->tx = off;
+  off = align_up(off + na * L->row_x * sizeof(float), 256);
+  L->ty = off;
+  off = align_up(off + na * L->row_y * sizeof(float), 256);
+  L->tz = off;
+  off = align_up(off + na * L->row_z * sizeof(float), 256);
+  L->supp = off;
+  off = align_up(off + na * 4 * sizeof(int32_t), 256);
+  L->total = off == 0 ? 256 : off;
+}
+
+int launch_tables(const vg_batch_desc* d, const vg_ws_layout& L, char* ws, cudaStream_t st) {
+  if (d->n_atoms == 0) return VG_OK;
+  TableParams p;
+  memset(&p, 0, sizeof p);
+  p.offsets = d->offsets;
+  p.xyz = d->xyz;
+  p.channel = d->channel;
+  p.mol_origin = d->mol_origin;
+  p.mol_delta = d->mol_delta;
+  p.tbl[0] = reinterpret_cast<float*>(ws + L.tx);
+  p.tbl[1] = reinterpret_cast<float*>(ws + L.ty);
+  p.tbl[2] = reinterpret_cast<float*>(ws + L.tz);
+  p.supp = reinterpret_cast<int32_t*>(ws + L.supp);
+  for (int a = 0; a < 3; ++a) {
+    p.origin[a] = d->origin[a];
+    p.delta[a] = d->delta[a];
+  }
+  p.scale = d->scale;
+  p.n_atoms = d->n_atoms;
+  p.n_molecules = d->n_molecules;
+  p.n[0] = d->W;
+  p.n[1] = d->H;
+  p.n[2] = d->D;
+  p.row[0] = L.row_x;
+  p.row[1] = L.row_y;
+  p.row[2] = L.row_z;
+  p.has_threshold = !std::isnan(d->threshold);
+  p.threshold = d->threshold;
+  p.periodic = d->periodic != 0;
+  const int64_t warps = d->n_atoms * 3;
+  const int64_t blocks = (warps + kTableThreads / 32 - 1) / (kTableThreads / 32);
+  vg_tables_kernel<<<(unsigned)blocks, kTableThreads, 0, st>>>(p);
+  return check_launch("vg_tables_kernel");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+VG_API const char* vg_last_error(void) { return g_last_error; }
+
+VG_API int vg_abi_version(void) { return VG_ABI_VERSION; }
+
+VG_API int vg_workspace_layout(const vg_batch_desc* desc, vg_ws_layout* layout) {
+  g_last_error[0] = '\0';
+  int rc = validate(desc);
+  if (rc != VG_OK) return rc;
+  if (layout == nullptr) return set_error(VG_ERR_INVALID, "layout is NULL");
+  fill_layout(desc, layout);
+  return VG_OK;
+}
+
+VG_API int vg_axis_tables_f32(const vg_batch_desc* desc, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  g_last_error[0] = '\0';
+  int rc = validate(desc);
+  if (rc != VG_OK) return rc;
+  vg_ws_layout L;
+  fill_layout(desc, &L);
+  if (workspace == nullptr || workspace_bytes < L.total)
+    return set_error(VG_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.total,
+                     workspace_bytes);
+  return launch_tables(desc, L, static_cast<char*>(workspace), static_cast<cudaStream_t>(stream));
+}
+
+namespace {
+
+// K3 launch (tables must already be in the workspace, same stream).
+int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
+                 vg_mol_stats* stats, cudaStream_t st) {
+  const bool vec = (d.D % 4) == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  const int64_t slab = (int64_t)d.W * d.D;
+  const int width = vec ? 4 : 1;
+  const int64_t nslots64 = slab / width;
+  if (nslots64 > INT_MAX / 2) return set_error(VG_ERR_INVALID, "slab W*D too large");
+  const int nslots = (int)nslots64;
+  // threads per CTA and slot steps per thread: NT <= 256, M <= 16, then
+  // split huge slabs into several CTAs (slot blocks)
+  int m_steps = 1;
+  while (m_steps < 16 && (nslots + m_steps - 1) / m_steps > kMaxThreads) m_steps *= 2;
+  int nt = (nslots + m_steps - 1) / m_steps;
+  nt = nt > kMaxThreads ? kMaxThreads : ((nt + 31) / 32) * 32;
+  const int per_block = nt * m_steps;
+  const int slot_blocks = (nslots + per_block - 1) / per_block;
+  // y-slabs per task: aim for >= 64 KiB of output per CTA
+  const int64_t bytes_per_slab_task = (int64_t)per_block * width * 4;
+  int jc = (int)((65536 + bytes_per_slab_task - 1) / bytes_per_slab_task);
+  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
+  const int n_jchunks = (d.H + jc - 1) / jc;
+  const int64_t tasks = d.n_molecules * d.C * (int64_t)n_jchunks * slot_blocks;
+  if (tasks > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)tasks);
+
+  if (stats != nullptr) {
+    cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * d.n_molecules, st);
+    if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
+  }
+  SlabParams p;
+  memset(&p, 0, sizeof p);
+  p.offsets = d.offsets;
+  p.tx = reinterpret_cast<const float*>(ws + L.tx);
+  p.ty = reinterpret_cast<const float*>(ws + L.ty);
+  p.tz = reinterpret_cast<const float*>(ws + L.tz);
+  p.supp = reinterpret_cast<const int4*>(ws + L.supp);
+  p.out = out;
+  p.stats = stats;
+  p.slab_elems = slab;
+  p.rx = L.row_x;
+  p.ry = L.row_y;
+  p.rz = L.row_z;
+  p.H = d.H;
+  p.C = d.C;
+  p.jc = jc;
+  p.n_jchunks = n_jchunks;
+  p.slot_blocks = slot_blocks;
+  p.nslots = nslots;
+  p.slots_per_row = vec ? d.D / 4 : d.D;
+  p.m_steps = m_steps;
+  if (vec)
+    vg_slab_kernel<true><<<(unsigned)tasks, nt, 0, st>>>(p);
+  else
+    vg_slab_kernel<false><<<(unsigned)tasks, nt, 0, st>>>(p);
+  return check_launch("vg_slab_kernel");
+}
+
+int prepare(const vg_batch_desc* desc, float* out, void* workspace, size_t workspace_bytes,
+            vg_ws_layout* L) {
+  g_last_error[0] = '\0';
+  int rc = validate(desc);
+  if (rc != VG_OK) return rc;
+  if (desc->n_molecules > 0 && out == nullptr) return set_error(VG_ERR_INVALID, "out is NULL");
+  fill_layout(desc, L);
+  if (workspace == nullptr || workspace_bytes < L->total)
+    return set_error(VG_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L->total,
+                     workspace_bytes);
+  return VG_OK;
+}
+
+}  // namespace
+
+VG_API int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspace,
+                           size_t workspace_bytes, vg_mol_stats* stats, void* stream) {
+  vg_ws_layout L;
+  int rc = prepare(desc, out, workspace, workspace_bytes, &L);
+  if (rc != VG_OK || desc->n_molecules == 0) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  rc = launch_tables(desc, L, ws, st);
+  if (rc != VG_OK) return rc;
+  return launch_slabs(*desc, L, ws, out, stats, st);
+}
+
+VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, const void* workspace,
+                        size_t workspace_bytes, vg_mol_stats* stats, void* stream) {
+  vg_ws_layout L;
+  int rc = prepare(desc, out, const_cast<void*>(workspace), workspace_bytes, &L);
+  if (rc != VG_OK || desc->n_molecules == 0) return rc;
+  return launch_slabs(*desc, L, static_cast<char*>(const_cast<void*>(workspace)), out, stats,
+                      static_cast<cudaStream_t>(stream));
+}
+
+VG_API int vg_erf_f32(const float* t, float* out, int64_t n, void* stream) {
+  g_last_error[0] = '\0';
+  if (n < 0) return set_error(VG_ERR_INVALID, "negative length");
+  if (n == 0) return VG_OK;
+  if (t == nullptr || out == nullptr) return set_error(VG_ERR_INVALID, "NULL pointer");
+  const int64_t blocks64 = (n + 255) / 256;
+  const unsigned blocks = (unsigned)(blocks64 > 148 * 64 ? 148 * 64 : blocks64);
+  vg_erf_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(t, out, n);
+  return check_launch("vg_erf_kernel");
+}
+
+VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
+  g_last_error[0] = '\0';
+  if (n < 0) return set_error(VG_ERR_INVALID, "negative length");
+  if (n == 0) return VG_OK;
+  if (out == nullptr || (reinterpret_cast<uintptr_t>(out) % 16) != 0)
+    return set_error(VG_ERR_INVALID, "out must be non-NULL and 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n4 = n / 4;
+  if (n4 > 0) {
+    int64_t blocks = (n4 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    vg_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(out), n4,
+                                                      make_float4(value, value, value, value));
+  }
+  const int64_t tail = n - n4 * 4;
+  if (tail > 0) vg_fill_tail_kernel<<<1, 32, 0, st>>>(out + n4 * 4, tail, value);
+  return check_launch("vg_fill_kernel");
+}
+
+VG_API int vg_exp_f32_host(const float* x, float* out, size_t n) {
+  if (n > 0 && (x == nullptr || out == nullptr)) return set_error(VG_ERR_INVALID, "NULL pointer");
+  for (size_t i = 0; i < n; ++i) out[i] = vg_exp_f32(x[i]);
+  return VG_OK;
+}
+
+VG_API int vg_erf_f32_host(const float* t, float* out, size_t n) {
+  if (n > 0 && (t == nullptr || out == nullptr)) return set_error(VG_ERR_INVALID, "NULL pointer");
+  for (size_t i = 0; i < n; ++i) out[i] = vg_erf_f32(t[i]);
+  return VG_OK;
+}

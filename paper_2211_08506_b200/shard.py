@@ -1,0 +1,54 @@
+"""Molecule sharding across GPUs (one process per GPU, no collective).
+
+Each molecule's grid depends only on its own atoms (reference gridgen.py:
+192-201; SPEC "batch parallelism is across grids only"), so a batch splits
+into contiguous molecule ranges, one per rank, with no exchange step. Ranges
+are balanced by an estimated per-molecule cost: output bytes dominate
+(every voxel is written once), plus a term for the atoms' pair work.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["molecule_costs", "plan_shards", "shard_range"]
+
+
+def molecule_costs(atom_counts, grid_bytes: int, bytes_per_atom: float = 0.0) -> np.ndarray:
+    """Relative cost of each molecule: grid bytes + ``bytes_per_atom`` x atoms."""
+    counts = np.asarray(atom_counts, dtype=np.float64)
+    return float(grid_bytes) + bytes_per_atom * counts
+
+
+def plan_shards(costs, world_size: int) -> list:
+    """Split molecules into ``world_size`` contiguous ``(start, stop)`` ranges
+    whose summed costs are as equal as prefix sums allow. Deterministic: every
+    rank computes the same plan from the same costs."""
+    if world_size < 1:
+        raise ValueError(f"world_size must be >= 1, got {world_size}")
+    costs = np.asarray(costs, dtype=np.float64).reshape(-1)
+    n = len(costs)
+    if n == 0:
+        return [(0, 0)] * world_size
+    prefix = np.concatenate([[0.0], np.cumsum(costs)])
+    total = prefix[-1]
+    cuts = [0]
+    for r in range(1, world_size):
+        target = total * r / world_size
+        k = int(np.searchsorted(prefix, target, side="left"))
+        # pick the closer of the two neighbouring cut points
+        if k > 0 and abs(prefix[k - 1] - target) <= abs(prefix[min(k, n)] - target):
+            k -= 1
+        cuts.append(min(max(k, cuts[-1]), n))
+    cuts.append(n)
+    return [(cuts[r], cuts[r + 1]) for r in range(world_size)]
+
+
+def shard_range(n_molecules: int, rank: int, world_size: int, costs=None) -> range:
+    """This rank's molecule indices (equal counts unless ``costs`` is given)."""
+    if not 0 <= rank < world_size:
+        raise ValueError(f"rank {rank} outside world of {world_size}")
+    if costs is None:
+        costs = np.ones(n_molecules)
+    start, stop = plan_shards(costs, world_size)[rank]
+    return range(start, stop)

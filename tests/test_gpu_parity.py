@@ -1,0 +1,352 @@
+"""Parity of the sm_100a path against the reference (golden fixtures made by
+the real reference) and against the CPU oracle on the same seeded inputs.
+
+The bar is bit-exact float32 grids (which implies the north_star tolerance
+|gpu - ref| <= 1e-6 + 1e-5 |ref|, reported on failure) and identical
+GenStats counters. Every call goes through the C-ABI library.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from _golden import (assert_bitwise, config_records, erf_cases, grid_cases, packed_sha, sha,
+                     table_cases)
+from oracle import voxgrid_oracle as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2211_08506_b200 as vg  # noqa: E402
+from paper_2211_08506_b200 import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    vg._native.lib()
+    yield
+    torch.cuda.synchronize()
+
+
+def spec_of(cfg):
+    return vg.GridSpec(cfg.shape, cfg.channels, vg.BoundingBox(cfg.box_origin, cfg.box_extents),
+                       cfg.sigma)
+
+
+def geom_of(cfg):
+    return orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents, cfg.sigma)
+
+
+# ---------------------------------------------------------------------------
+# numerics
+# ---------------------------------------------------------------------------
+def test_device_erf_matches_golden():
+    t, e = erf_cases()
+    got = vg.erf_approx(t)
+    assert np.array_equal(got.view(np.uint32), e.view(np.uint32))
+
+
+def test_device_erf_all_floats_0_to_6_vs_oracle():
+    hi = int(np.float32(6.0).view(np.uint32))
+    step = 1 << 25
+    for s in range(0, hi + 1, step):
+        bits = torch.arange(s, min(s + step, hi + 1), dtype=torch.int64, device="cuda")
+        t = bits.to(torch.int32).view(torch.float32)
+        got = vg.erf_approx(t).cpu().numpy()
+        tn = t.cpu().numpy()
+        with np.errstate(all="ignore"):
+            ref = orc.erf_f32(tn)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), hex(s)
+        neg = vg.erf_approx(-t).cpu().numpy()
+        assert np.array_equal(neg, -got)
+
+
+@pytest.mark.parametrize("case", range(len(table_cases())))
+def test_axis_tables_match_golden(case):
+    meta, values = table_cases()[case]
+    tabs = vg.fused_axis_tables(meta["mus"], meta["params"], meta["sigma"],
+                                threshold=meta["threshold"], periodic=meta["periodic"])
+    for a in range(3):
+        assert np.array_equal(tabs[a].values.view(np.uint32), values[a].view(np.uint32)), (case, a)
+        assert list(tabs[a].support) == meta["supports"][a], (case, a)
+
+
+# ---------------------------------------------------------------------------
+# single grids: the reference's KAT-style cases
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("idx", range(len(grid_cases())))
+def test_generate_grid_matches_golden(idx):
+    m, g = grid_cases()[idx]
+    lattice = vg.LatticeCell(tuple(m["periodic"])) if m["periodic"] else None
+    spec = vg.GridSpec(tuple(m["shape"]), m["channels"],
+                       vg.BoundingBox(tuple(m["origin"]), tuple(m["extents"])), m["sigma"],
+                       lattice)
+    ps = vg.ParticleSet(np.array(m["chans"], dtype=np.int64),
+                        np.array(m["pos"]).reshape(-1, 3), lattice)
+    grid, st = vg.generate_grid(ps, spec, mode=m["mode"], threshold=m["threshold"])
+    assert grid.data.is_cuda and grid.data.dtype == torch.float32
+    assert_bitwise(grid.numpy(), g, m["name"])
+    assert (st.voxel_writes, st.erf_evals, st.nonzero_voxels) == (
+        m["voxel_writes"], m["erf_evals"], m["nonzero_voxels"]), m["name"]
+
+
+def test_layout_contract_argmax():
+    # reference test_core.py:131-142
+    spec = vg.GridSpec((2, 3, 4), 1, vg.BoundingBox((0, 0, 0), (3, 2, 4)), 0.08)
+    grid, _ = vg.generate_grid(vg.ParticleSet([0], [[2.5, 0.5, 3.5]]), spec)
+    data = grid.numpy()
+    assert data.shape == (1, 2, 3, 4)
+    assert np.unravel_index(np.argmax(data), data.shape) == (0, 0, 2, 3)
+    assert grid.value_at(0, (2, 0, 3)) == data[0, 0, 2, 3]
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs: golden hashes from the real reference
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("rec_i", range(len(config_records()["batches"])))
+def test_config_batches_match_golden(rec_i):
+    rec = config_records()["batches"][rec_i]
+    cfg = synth.CONFIGS[rec["config"]]
+    pb = synth.packed_batch(cfg, rec["indices"])
+    assert packed_sha(pb) == rec["inputs_sha"]
+    spec = spec_of(cfg)
+    if rec["spec_policy"] == "fixed":
+        grids, stats = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+        stats = stats.cpu().numpy()
+        host = grids.cpu().numpy()
+        for b, g in enumerate(rec["grids"]):
+            assert sha(host[b]) == g["sha"], (rec["config"], rec["indices"][b])
+            assert stats[b, 0] == g["voxel_writes"] and stats[b, 1] == g["nonzero_voxels"]
+    else:
+        sets = [vg.ParticleSet(*pb.molecule(b)) for b in range(pb.n_molecules)]
+        res = vg.generate_batch(sets, spec, spec_policy=rec["spec_policy"])
+        assert not res.errors
+        for (grid, st), g in zip(res.results, rec["grids"]):
+            assert [list(grid.spec.box.origin), list(grid.spec.box.extents)] == g["box"]
+            assert sha(grid.numpy()) == g["sha"]
+            assert (st.voxel_writes, st.erf_evals, st.nonzero_voxels) == (
+                g["voxel_writes"], g["erf_evals"], g["nonzero_voxels"])
+
+
+def test_estimator_matches_golden():
+    from paper_2211_08506_b200 import GaussianVoxelizer
+
+    rec = config_records()["estimator"]
+    clouds = []
+    for b in range(6):
+        ch, xyz = synth.molecule(synth.CONFIGS[0], b)
+        clouds.append(np.column_stack([ch.astype(np.float64), xyz]))
+    est = GaussianVoxelizer(grid_size=24, sigma=0.4).fit(clouds)
+    assert est.channels_ == rec["shared"]["channels"]
+    assert [list(est.box_.origin), list(est.box_.extents)] == rec["shared"]["box"]
+    out = est.transform(clouds)
+    assert out.is_cuda and tuple(out.shape) == (6, est.channels_, 24, 24, 24)
+    host = out.cpu().numpy()
+    assert [sha(g) for g in host] == rec["shared"]["shas"]
+    per = GaussianVoxelizer(grid_size=(20, 16, 12), sigma=0.5, box="per-sample").fit(clouds)
+    assert [sha(g) for g in per.transform(clouds).cpu().numpy()] == rec["per_sample"]["shas"]
+
+
+# ---------------------------------------------------------------------------
+# full configs vs the oracle on this host
+# ---------------------------------------------------------------------------
+def _compare_with_oracle(cfg, indices, workers=None):
+    pb = synth.packed_batch(cfg, indices)
+    grids, stats = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec_of(cfg))
+    ref, ref_stats = orc.batch(pb.offsets, pb.channels, pb.xyz, geom_of(cfg),
+                               workers=workers or orc.host_cores())
+    assert_bitwise(grids.cpu().numpy(), ref, cfg.name)
+    st = stats.cpu().numpy()
+    assert [int(v) for v in st[:, 0]] == [r["voxel_writes"] for r in ref_stats]
+    assert [int(v) for v in st[:, 1]] == [r["nonzero_voxels"] for r in ref_stats]
+
+
+def test_cfg0_full_vs_oracle():
+    _compare_with_oracle(synth.CONFIGS[0], range(64))
+
+
+def test_cfg1_full_vs_oracle():
+    cfg = synth.CONFIGS[1]
+    for start in range(0, cfg.n_molecules, 256):
+        _compare_with_oracle(cfg, range(start, start + 256))
+
+
+def test_cfg2_strided_sample_vs_oracle():
+    _compare_with_oracle(synth.CONFIGS[2], range(7, 65536, 97))
+
+
+def test_cfg3_full_vs_oracle():
+    cfg = synth.CONFIGS[3]
+    for start in range(0, cfg.n_molecules, 8):
+        _compare_with_oracle(cfg, range(start, start + 8))
+
+
+def test_cfg4_full_vs_oracle():
+    cfg = synth.CONFIGS[4]
+    for start in range(0, cfg.n_molecules, 1024):
+        _compare_with_oracle(cfg, range(start, start + 1024))
+
+
+# ---------------------------------------------------------------------------
+# size-independent properties at full size
+# ---------------------------------------------------------------------------
+def _digest(t):
+    flat = t.reshape(t.shape[0], -1).view(torch.int32).to(torch.int64)
+    w = torch.arange(1, flat.shape[1] + 1, device=t.device, dtype=torch.int64)
+    return ((flat * w).sum(dim=1) % (2**61 - 1)).cpu().numpy()
+
+
+def test_cfg2_full_chunking_invariant_and_nonzero_counts():
+    """All 65,536 cfg2 grids: per-grid digests are identical whether the batch
+    is launched in chunks of 8192 or 5000 molecules (output independent of
+    launch shape), and the kernel's nonzero counters equal torch's count."""
+    cfg = synth.CONFIGS[2]
+    pb = synth.packed_batch(cfg)
+    spec = spec_of(cfg)
+
+    def run(chunk):
+        digs, nz = [], []
+        for s in range(0, pb.n_molecules, chunk):
+            e = min(s + chunk, pb.n_molecules)
+            lo, hi = pb.offsets[s], pb.offsets[e]
+            g, st = vg.generate_packed(pb.offsets[s:e + 1] - lo, pb.channels[lo:hi],
+                                       pb.xyz[lo:hi], spec)
+            digs.append(_digest(g))
+            cnt = (g.reshape(e - s, -1) != 0).sum(dim=1).cpu().numpy()
+            assert np.array_equal(cnt, st[:, 1].cpu().numpy())
+            nz.append(cnt)
+            del g
+        return np.concatenate(digs), np.concatenate(nz)
+
+    d1, n1 = run(8192)
+    d2, n2 = run(5000)
+    assert np.array_equal(d1, d2) and np.array_equal(n1, n2)
+
+
+def test_normalization_with_margin():
+    # reference acceptance c01 (test_acceptance.py:59-74): mass == atom count
+    rng = np.random.default_rng(20240817)
+    for trial in range(20):
+        sigma = float(rng.choice([0.05, 0.1, 0.25, 0.5]))
+        ext = float(rng.uniform(7.0, 12.0))
+        origin = rng.uniform(-3, 3, 3)
+        n = int(rng.integers(1, 9))
+        pos = origin + 2.0 + rng.uniform(0, ext - 4.0, (n, 3))
+        ch = rng.integers(0, 3, n)
+        spec = vg.GridSpec((24, 24, 24), 3, vg.BoundingBox(tuple(origin), (ext,) * 3), sigma)
+        grid, _ = vg.generate_grid(vg.ParticleSet(ch, pos), spec)
+        sums = grid.channel_sums()
+        counts = np.bincount(ch, minlength=3)
+        assert abs(sums.sum() - n) <= 1e-3 * n
+        for c in range(3):
+            assert abs(sums[c] - counts[c]) <= max(1e-3 * counts[c], 1e-6)
+
+
+def test_translation_equivariance_bitwise():
+    spec = vg.GridSpec((16, 16, 16), 1, vg.BoundingBox((0, 0, 0), (8, 8, 8)), 0.5)
+    base_pos = np.array([[2.25, 3.5, 4.125], [5.0, 2.75, 6.5]])
+    base, _ = vg.generate_grid(vg.ParticleSet([0, 0], base_pos), spec)
+    for shift in [(1.5, -2.25, 4.0), (0.1, 0.37, -1.234), (-2.9, 1.7, 0.3)]:
+        moved = vg.GridSpec((16, 16, 16), 1, spec.box.translate(shift), 0.5)
+        g, _ = vg.generate_grid(vg.ParticleSet([0, 0], base_pos + np.asarray(shift)), moved)
+        assert torch.equal(g.data, base.data)
+
+
+# ---------------------------------------------------------------------------
+# edge cases and errors
+# ---------------------------------------------------------------------------
+def test_empty_batch_and_empty_molecules():
+    spec = vg.GridSpec((8, 8, 8), 2, vg.BoundingBox((0, 0, 0), (4, 4, 4)), 0.3)
+    res = vg.generate_batch([], spec)
+    assert tuple(res.tensor.shape) == (0, 2, 8, 8, 8)
+    sets = [vg.ParticleSet.from_rows([]), vg.ParticleSet([1], [[2, 2, 2]]),
+            vg.ParticleSet.from_rows([])]
+    res = vg.generate_batch(sets, spec)
+    assert not res.errors
+    t = res.tensor.cpu().numpy()
+    assert not t[0].any() and not t[2].any() and t[1, 1].sum() > 0.99
+    ref, _ = orc.grid([1], [[2, 2, 2]], orc.Geometry((8, 8, 8), 2, (0, 0, 0), (4, 4, 4), 0.3))
+    assert_bitwise(t[1], ref)
+
+
+def test_per_index_errors_do_not_abort_batch():
+    spec = vg.GridSpec((8, 8, 8), 1, vg.BoundingBox((0, 0, 0), (4, 4, 4)), 0.3)
+    good = vg.ParticleSet([0], [[2, 2, 2]])
+    bad = vg.ParticleSet([5], [[2, 2, 2]])
+    res = vg.generate_batch([good, bad, good], spec)
+    assert list(res.errors) == [1]
+    assert res.results[0] is not None and res.results[2] is not None and res.results[1] is None
+    assert not res.tensor[1].any()
+    with pytest.raises(ValueError):
+        res.grids()
+    with pytest.raises(ValueError):
+        vg.generate_grid(bad, spec)
+
+
+def test_periodicity_mismatch_errors():
+    cell = vg.LatticeCell((6.0, 6.0, 6.0))
+    spec = vg.GridSpec((8, 8, 8), 1, vg.BoundingBox((0, 0, 0), (6, 6, 6)), 0.3, cell)
+    with pytest.raises(ValueError):
+        vg.generate_grid(vg.ParticleSet([0], [[1, 1, 1]]), spec)
+    open_spec = vg.GridSpec((8, 8, 8), 1, vg.BoundingBox((0, 0, 0), (6, 6, 6)), 0.3)
+    with pytest.raises(ValueError):
+        vg.generate_grid(vg.ParticleSet([0], [[1, 1, 1]], cell), open_spec)
+
+
+def test_dense_mode_counts_and_bits():
+    spec = vg.GridSpec((16, 16, 16), 1, vg.BoundingBox((0, 0, 0), (6, 6, 6)), 0.2)
+    rng = np.random.default_rng(19)
+    ps = vg.ParticleSet(np.zeros(5, int), rng.uniform(0, 6, (5, 3)))
+    gs, ss = vg.generate_grid(ps, spec, mode="sparse")
+    gd, sd = vg.generate_grid(ps, spec, mode="dense")
+    assert torch.equal(gs.data, gd.data)
+    assert sd.voxel_writes == 5 * 16**3 and ss.voxel_writes <= sd.voxel_writes
+    with pytest.raises(ValueError):
+        vg.generate_grid(ps, spec, mode="fast")
+    with pytest.raises(ValueError):
+        vg.generate_grid(ps, spec, dtype=np.float64)
+
+
+def test_candidate_list_overflow_path_vs_oracle():
+    """A 3000-atom single-channel molecule in a small box: every y-chunk has
+    > 1024 candidate atoms, exercising the segmented list path."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    xyz = rng.uniform(0, 6, (n, 3))
+    ch = np.zeros(n, np.int32)
+    ch[::7] = 1
+    spec = vg.GridSpec((20, 24, 28), 2, vg.BoundingBox((0, 0, 0), (6, 6, 6)), 0.6)
+    grids, st = vg.generate_packed(np.array([0, n]), ch, xyz, spec)
+    ref, rs = orc.grid(ch, xyz, orc.Geometry((20, 24, 28), 2, (0, 0, 0), (6, 6, 6), 0.6))
+    assert_bitwise(grids[0].cpu().numpy(), ref, "overflow")
+    assert int(st[0, 0]) == rs["voxel_writes"] and int(st[0, 1]) == rs["nonzero_voxels"]
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 7), (5, 3, 4), (33, 31, 36), (4, 70, 8)])
+def test_odd_shapes_vs_oracle(shape):
+    rng = np.random.default_rng(sum(shape))
+    n = 9
+    ext = (3.0, 2.5, 4.0)
+    xyz = rng.uniform(-0.5, 4.0, (n, 3))
+    ch = rng.integers(0, 3, n).astype(np.int32)
+    spec = vg.GridSpec(shape, 3, vg.BoundingBox((0, 0, 0), ext), 0.35)
+    grids, st = vg.generate_packed(np.array([0, 4, n]), ch, xyz, spec)
+    geom = orc.Geometry(shape, 3, (0, 0, 0), ext, 0.35)
+    ref, rs = orc.batch(np.array([0, 4, n]), ch, xyz, geom)
+    assert_bitwise(grids.cpu().numpy(), ref, str(shape))
+    assert [int(v) for v in st[:, 1].cpu()] == [r["nonzero_voxels"] for r in rs]
+
+
+def test_out_tensor_and_stream():
+    cfg = synth.CONFIGS[0]
+    pb = synth.packed_batch(cfg, range(4))
+    spec = spec_of(cfg)
+    out = torch.full((4, 5, 32, 32, 32), 7.0, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec, out=out, with_stats=False)
+    s.synchronize()
+    ref, _ = orc.batch(pb.offsets, pb.channels, pb.xyz, geom_of(cfg))
+    assert_bitwise(out.cpu().numpy(), ref, "out=")

@@ -1,0 +1,109 @@
+"""The C-ABI library on a CPU-only host: it loads, exports every symbol the
+public header declares, and its host build of the device numerics (shared
+source csrc/vg_math.cuh) reproduces numpy's float32 exp and the reference
+erf bit for bit. No compute call touches a GPU here."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from _golden import erf_cases
+from oracle import voxgrid_oracle as orc
+from paper_2211_08506_b200 import _native
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "voxgrid_b200.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _native.build_native()
+    return _native.lib()
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(vg_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_api():
+    names = declared_functions()
+    for must in ("vg_generate_f32", "vg_workspace_layout", "vg_axis_tables_f32", "vg_erf_f32",
+                 "vg_exp_f32_host", "vg_erf_f32_host", "vg_last_error", "vg_abi_version",
+                 "vg_fill_f32"):
+        assert must in names
+    assert set(names) == set(_native.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.vg_abi_version() == _native.ABI_VERSION
+
+
+def _host(fn, x):
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    assert fn(x.ctypes.data, out.ctypes.data, x.size) == 0
+    return out
+
+
+def test_host_exp_matches_numpy_sample_of_all_floats(lib):
+    bits = np.arange(0, 2**32, 61, dtype=np.uint64).astype(np.uint32)
+    x = bits.view(np.float32)
+    with np.errstate(all="ignore"):
+        ref = np.exp(x)
+    got = _host(lib.vg_exp_f32_host, x)
+    same = (got.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(got) & np.isnan(ref))
+    assert same.all(), f"{(~same).sum()} mismatches, first at {x[~same][:4]}"
+
+
+def test_host_exp_matches_numpy_on_erf_domain(lib):
+    # y = -t*t in (-17, 0] is where exp's bits reach the Bürmann erf
+    lo = int(np.float32(-17.0).view(np.uint32))
+    bits = np.arange(0x80000000, lo + 1, 13, dtype=np.uint64).astype(np.uint32)
+    x = bits.view(np.float32)
+    assert np.array_equal(_host(lib.vg_exp_f32_host, x).view(np.uint32),
+                          np.exp(x).view(np.uint32))
+
+
+def test_host_erf_matches_golden_reference_values(lib):
+    t, e = erf_cases()
+    assert np.array_equal(_host(lib.vg_erf_f32_host, t).view(np.uint32), e.view(np.uint32))
+
+
+def test_host_erf_matches_oracle_dense_range(lib):
+    hi = int(np.float32(6.0).view(np.uint32))
+    t = np.arange(0, hi, 37, dtype=np.uint32).view(np.float32)
+    t = np.concatenate([t, -t])
+    with np.errstate(all="ignore"):
+        ref = orc.erf_f32(t)
+    assert np.array_equal(_host(lib.vg_erf_f32_host, t).view(np.uint32), ref.view(np.uint32))
+
+
+def test_erf_saturates_exactly(lib):
+    # reference test_kernels.py:54 — erf(5.0f) == 1.0f exactly; odd symmetry exact
+    t = np.array([5.0, -5.0, 0.0, -0.0, 9.0], dtype=np.float32)
+    got = _host(lib.vg_erf_f32_host, t)
+    assert got[0] == 1.0 and got[1] == -1.0 and got[2] == 0.0 and got[4] == 1.0
+
+
+def test_invalid_descriptor_reports_error_without_gpu(lib):
+    d = _native.VgBatchDesc()
+    d.n_molecules, d.n_atoms = 1, 0
+    d.H = d.W = d.D = 0
+    d.C = 1
+    d.scale = 1.0
+    layout = _native.VgWsLayout()
+    rc = lib.vg_workspace_layout(ctypes.byref(d), ctypes.byref(layout))
+    assert rc == -1
+    assert b"shape" in lib.vg_last_error()
+    d.H = d.W = d.D = 8
+    d.delta[:] = (0.5, 0.5, 0.5)
+    d.offsets = 8  # any non-NULL pointer; layout never dereferences it
+    assert lib.vg_workspace_layout(ctypes.byref(d), ctypes.byref(layout)) == 0
+    assert layout.total >= 256 and layout.row_x == 8
