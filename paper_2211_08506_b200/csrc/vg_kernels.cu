@@ -28,6 +28,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/voxgrid_b200.h"
@@ -55,8 +56,11 @@ int check_launch(const char* what) {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
-constexpr int kListCap = 1024;       // K3: candidate segment capacity
-constexpr int kMaxThreads = 256;     // K3: threads per CTA (upper bound)
+constexpr int kListCap = 256;        // K3: candidate segment capacity
+constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
+constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bound)
+constexpr int kStageBytes = 16384;
+constexpr int64_t kTaskBytes = 262144; // K3: output bytes per CTA (y-chunk sizing)   // K3: shared-memory staging budget per CTA
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -202,13 +206,24 @@ struct SlabParams {
   vg_mol_stats* stats;
   int64_t slab_elems;   // W*D
   int rx, ry, rz;       // table row strides
-  int H, C;
+  int H, W, C;
   int jc;               // y-slabs per task
   int n_jchunks;
+  // generic kernel
   int slot_blocks;      // CTAs per slab along the slot axis
   int nslots;           // slots per slab (float4 or float)
-  int slots_per_row;    // D/4 (vector) or D (scalar)
   int m_steps;          // slot steps per thread per slab
+  // both
+  int slots_per_row;    // D/4 (vector) or D (scalar)
+  // row-structured kernel
+  int row_blocks;       // CTAs per slab along x rows
+  int rows_per_step;    // R = blockDim.x / slots_per_row
+  unsigned long long spr_magic;  // floor(2^32 / slots_per_row) + 1
+  int stage_cap;        // candidates that fit the shared-memory staging area
+  int stage_stride;     // floats per staged candidate: gy[pad4(jc)] gx[pad4(W)] gz[pad4(D)]
+  int stage_gx;         // offset of gx inside a staged block
+  int stage_gz;         // offset of gz inside a staged block
+  int stage_floats;     // floats of the staging area (sublists follow it)
 };
 
 struct SlabShared {
@@ -222,10 +237,11 @@ __device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
 
 // Block-wide ordered compaction: scans atoms [pos, a1) in rounds of
 // blockDim.x and appends, in ascending atom order, every atom of channel c
-// with a non-empty support box whose y-support meets [jlo, jhi). Stops once
-// at least kListCap entries are held; `pos` returns the resume point.
-__device__ int build_list(const SlabParams& p, SlabShared& sh, int64_t& pos, int64_t a1, int c,
-                          int jlo, int jhi) {
+// with a non-empty support box whose y-support meets [jlo, jhi) and whose
+// x-support meets [xa, xb). Stops once at least kListCap entries are held;
+// `pos` returns the resume point.
+__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t& pos, int64_t a1,
+                          int c, int jlo, int jhi, int xa, int xb) {
   const int nt = blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
   int count = 0;
@@ -234,9 +250,9 @@ __device__ int build_list(const SlabParams& p, SlabShared& sh, int64_t& pos, int
     bool keep = false;
     int4 s = make_int4(0, 0, 0, 0);
     if (idx < a1) {
-      s = __ldg(p.supp + idx);
+      s = __ldg(supp + idx);
       keep = s.w == c && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
-             hi16(s.y) > jlo;
+             hi16(s.y) > jlo && lo16(s.x) < xb && hi16(s.x) > xa;
     }
     const unsigned bal = __ballot_sync(kFull, keep);
     if (lane == 0) sh.warp_cnt[warp] = __popc(bal);
@@ -272,35 +288,17 @@ __device__ __forceinline__ int nonzeros(const float4& a) {
 }
 __device__ __forceinline__ int nonzeros(const float& a) { return a != 0.f; }
 
-// acc += fl32(pyx * gz) elementwise, never contracted to FMA.
+// acc += fl32(pyx * gz) elementwise, never contracted to FMA. `gzrow` may
+// point to shared or global memory (generic load).
 __device__ __forceinline__ void add_terms(float4& acc, float pyx, const float* gzrow, int k) {
-  const float4 gz = __ldg(reinterpret_cast<const float4*>(gzrow) + k);
+  const float4 gz = reinterpret_cast<const float4*>(gzrow)[k];
   acc.x = VG_FADD(acc.x, VG_FMUL(pyx, gz.x));
   acc.y = VG_FADD(acc.y, VG_FMUL(pyx, gz.y));
   acc.z = VG_FADD(acc.z, VG_FMUL(pyx, gz.z));
   acc.w = VG_FADD(acc.w, VG_FMUL(pyx, gz.w));
 }
 __device__ __forceinline__ void add_terms(float& acc, float pyx, const float* gzrow, int k) {
-  acc = VG_FADD(acc, VG_FMUL(pyx, __ldg(gzrow + k)));
-}
-
-// Accumulates candidates meta[0..n) (ascending atom order) into one slot.
-template <bool VEC>
-__device__ __forceinline__ void gather_slot(const SlabParams& p, const int4* meta, int n, int j,
-                                            bool valid, int i, int k,
-                                            typename SlotT<VEC>::T& acc) {
-  for (int q = 0; q < n; ++q) {
-    const int4 s = meta[q];
-    if (j < lo16(s.y) || j >= hi16(s.y)) continue;  // uniform: y-support
-    const bool hit = valid && i >= lo16(s.x) && i < hi16(s.x);
-    if (!__any_sync(kFull, hit)) continue;           // uniform: warp rows miss x-support
-    if (valid) {
-      const int64_t a = s.w;
-      const float gy = __ldg(p.ty + a * p.ry + j);
-      const float pyx = VG_FMUL(gy, __ldg(p.tx + a * p.rx + i));  // multiply.outer(ty, tx)
-      add_terms(acc, pyx, p.tz + a * p.rz, k);                     // (.. ) outer tz, then +=
-    }
-  }
+  acc = VG_FADD(acc, VG_FMUL(pyx, gzrow[k]));
 }
 
 __device__ __forceinline__ void store_slot(float* slab, int f, const float4& v) {
@@ -320,8 +318,47 @@ __device__ long long block_sum(SlabShared& sh, long long v) {
   return t;  // valid in thread 0
 }
 
+// Per-molecule counters: nonzero voxels of this CTA (integer atomics are
+// order-independent) and, from one CTA per molecule, voxel_writes.
+__device__ void finish_stats(const SlabParams& p, SlabShared& sh, int64_t b, int64_t a0,
+                             int64_t a1, long long nz, bool owner) {
+  const long long tot = block_sum(sh, nz);
+  if (threadIdx.x == 0 && tot != 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[b].nonzero_voxels),
+              (unsigned long long)tot);
+  if (owner) {
+    // voxel_writes = sum of support-box volumes (gridgen.py:103)
+    long long w = 0;
+    for (int64_t a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
+      const int4 s = __ldg(p.supp + a);
+      w += (long long)(hi16(s.x) - lo16(s.x)) * (hi16(s.y) - lo16(s.y)) * (hi16(s.z) - lo16(s.z));
+    }
+    const long long wt = block_sum(sh, w);
+    if (threadIdx.x == 0) p.stats[b].voxel_writes = wt;
+  }
+}
+
+// --- generic kernel: any slab shape, one division per slot ------------------
 template <bool VEC>
-__global__ void __launch_bounds__(kMaxThreads) vg_slab_kernel(SlabParams p) {
+__device__ __forceinline__ void gather_slot(const SlabParams& p, const int4* meta, int n, int j,
+                                            bool valid, int i, int k,
+                                            typename SlotT<VEC>::T& acc) {
+  for (int q = 0; q < n; ++q) {
+    const int4 s = meta[q];
+    if (j < lo16(s.y) || j >= hi16(s.y)) continue;  // uniform: y-support
+    const bool hit = valid && i >= lo16(s.x) && i < hi16(s.x);
+    if (!__any_sync(kFull, hit)) continue;           // uniform: warp rows miss x-support
+    if (valid) {
+      const int64_t a = s.w;
+      const float gy = __ldg(p.ty + a * p.ry + j);
+      const float pyx = VG_FMUL(gy, __ldg(p.tx + a * p.rx + i));  // multiply.outer(ty, tx)
+      add_terms(acc, pyx, p.tz + a * p.rz, k);                     // (.. ) outer tz, then +=
+    }
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kMaxThreads) vg_slab_generic_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotT<VEC>::T;
   __shared__ SlabShared sh;
   const int nt = blockDim.x;
@@ -340,7 +377,7 @@ __global__ void __launch_bounds__(kMaxThreads) vg_slab_kernel(SlabParams p) {
   const int slot0 = sb * nt * p.m_steps;
 
   int64_t pos = a0;
-  const int n_list = build_list(p, sh, pos, a1, c, j0, j1);
+  const int n_list = build_list(p.supp, sh, pos, a1, c, j0, j1, 0, kMaxAxis);
   const bool single = pos >= a1;  // every candidate of the chunk fits the list
 
   float* out_c = p.out + ((b * p.C + c) * (int64_t)p.H) * p.slab_elems;
@@ -362,7 +399,7 @@ __global__ void __launch_bounds__(kMaxThreads) vg_slab_kernel(SlabParams p) {
         int64_t pos2 = a0;
         while (pos2 < a1) {
           __syncthreads();
-          const int n2 = build_list(p, sh, pos2, a1, c, j, j + 1);
+          const int n2 = build_list(p.supp, sh, pos2, a1, c, j, j + 1, 0, kMaxAxis);
           gather_slot<VEC>(p, sh.meta, n2, j, valid, i, k, acc);
         }
         __syncthreads();
@@ -373,23 +410,224 @@ __global__ void __launch_bounds__(kMaxThreads) vg_slab_kernel(SlabParams p) {
       }
     }
   }
+  if (p.stats != nullptr) finish_stats(p, sh, b, a0, a1, nz, c == 0 && chunk == 0 && sb == 0);
+}
 
-  if (p.stats != nullptr) {
-    const long long tot = block_sum(sh, nz);
-    if (threadIdx.x == 0 && tot != 0)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[b].nonzero_voxels),
-                (unsigned long long)tot);
-    if (c == 0 && chunk == 0 && sb == 0) {
-      // voxel_writes = sum of support-box volumes (gridgen.py:103)
-      long long w = 0;
-      for (int64_t a = a0 + threadIdx.x; a < a1; a += nt) {
-        const int4 s = __ldg(p.supp + a);
-        w += (long long)(hi16(s.x) - lo16(s.x)) * (hi16(s.y) - lo16(s.y)) * (hi16(s.z) - lo16(s.z));
+// --- row-structured kernel ----------------------------------------------------
+// Thread t owns slot k = t % spr of rows r0 + m*R (m < M, R = blockDim/spr):
+// no per-slot division, M accumulators in registers, candidates outer. A
+// warp's rows at step m are [wr0 + m*R, wr1 + m*R]; the warp skips a
+// candidate whose x-support misses them (uniform branch, exact: skipped terms
+// are +0). Grid = (molecule, channel, y-chunk x row-block).
+
+__device__ __forceinline__ int div_magic(int n, unsigned long long magic) {
+  return (int)(((unsigned long long)n * magic) >> 32);  // exact for n < 2^16, d < 2^16
+}
+
+__device__ __forceinline__ void add_scaled(float4& acc, float pyx, const float4& gz) {
+  acc.x = VG_FADD(acc.x, VG_FMUL(pyx, gz.x));
+  acc.y = VG_FADD(acc.y, VG_FMUL(pyx, gz.y));
+  acc.z = VG_FADD(acc.z, VG_FMUL(pyx, gz.z));
+  acc.w = VG_FADD(acc.w, VG_FMUL(pyx, gz.w));
+}
+__device__ __forceinline__ void add_scaled(float& acc, float pyx, const float& gz) {
+  acc = VG_FADD(acc, VG_FMUL(pyx, gz));
+}
+__device__ __forceinline__ void load_slot(float4& v, const float* row, int k) {
+  v = reinterpret_cast<const float4*>(row)[k];
+}
+__device__ __forceinline__ void load_slot(float& v, const float* row, int k) { v = row[k]; }
+__device__ __forceinline__ void ldg_slot(float4& v, const float* row, int k) {
+  v = __ldg(reinterpret_cast<const float4*>(row) + k);
+}
+__device__ __forceinline__ void ldg_slot(float& v, const float* row, int k) { v = __ldg(row + k); }
+
+// Explicit shared-space loads (32-bit addresses): keeps the hot loop free of
+// generic-to-shared address arithmetic.
+__device__ __forceinline__ float lds_f32(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int2 lds_int2(unsigned a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void lds_slot(float4& v, unsigned a) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+}
+__device__ __forceinline__ void lds_slot(float& v, unsigned a) { v = lds_f32(a); }
+// Nonzero count of values known to be >= +0 (sums of products of masses):
+// such a float is nonzero iff its bit pattern is.
+__device__ __forceinline__ int nonzeros_pos(const float4& a) {
+  return min(__float_as_int(a.x), 1) + min(__float_as_int(a.y), 1) + min(__float_as_int(a.z), 1) +
+         min(__float_as_int(a.w), 1);
+}
+__device__ __forceinline__ int nonzeros_pos(const float& a) { return min(__float_as_int(a), 1); }
+
+// Out-of-line path for chunks whose candidates do not fit the shared-memory
+// staging area (or exceed kListCap): tables are read through L1/L2 and the
+// list is rebuilt per slab in ascending segments. Returns the nonzero count.
+template <int M, bool VEC>
+__device__ __noinline__ int slab_rows_unstaged(const SlabParams& p, SlabShared& sh, int64_t b,
+                                               int c, int64_t a0, int64_t a1, int j0, int j1,
+                                               int row_base, int row_end, int r0, int k, int wr0,
+                                               int wr1) {
+  using Slot = typename SlotT<VEC>::T;
+  float* out_c = p.out + ((b * p.C + c) * (int64_t)p.H) * p.slab_elems;
+  const int R = p.rows_per_step, ibase = row_base + r0;
+  int nz = 0;
+  for (int j = j0; j < j1; ++j) {
+    Slot acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) zero_slot(acc[m]);
+    unsigned touched = 0;
+    int64_t pos = a0;
+    while (pos < a1) {
+      __syncthreads();
+      const int n = build_list(p.supp, sh, pos, a1, c, j, j + 1, row_base, row_end);
+      for (int q = 0; q < n; ++q) {
+        const int4 s = sh.meta[q];
+        const int64_t a = s.w;
+        const float gy = __ldg(p.ty + a * p.ry + j);
+        const float* gx = p.tx + a * p.rx;
+        Slot gz;
+        ldg_slot(gz, p.tz + a * p.rz, k);
+        const int dlo = lo16(s.x) - (row_base + wr1);
+        const int dhi = hi16(s.x) - (row_base + wr0);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int mr = m * R;
+          if (mr >= dlo && mr < dhi) {
+            const float pyx = VG_FMUL(gy, __ldg(gx + min(ibase + mr, p.W - 1)));
+            add_scaled(acc[m], pyx, gz);
+            touched |= 1u << m;
+          }
+        }
       }
-      const long long wt = block_sum(sh, w);
-      if (threadIdx.x == 0) p.stats[b].voxel_writes = wt;
+    }
+    __syncthreads();
+    float* slab = out_c + (int64_t)j * p.slab_elems;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int i = ibase + m * R;
+      if (i < row_end) {
+        store_slot(slab, i * p.slots_per_row + k, acc[m]);
+        if ((touched >> m) & 1u) nz += nonzeros(acc[m]);
+      }
     }
   }
+  return nz;
+}
+
+template <int M, bool VEC>
+__global__ void __launch_bounds__(kRowThreads, 4) vg_slab_kernel(const __grid_constant__ SlabParams p) {
+  using Slot = typename SlotT<VEC>::T;
+  __shared__ SlabShared sh;
+  extern __shared__ float4 stage4[];
+  float* stage = reinterpret_cast<float*>(stage4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+
+  const int64_t b = blockIdx.x;
+  const int c = blockIdx.y;
+  int chunk = blockIdx.z, rblk = 0;
+  if (p.row_blocks > 1) {
+    rblk = chunk % p.row_blocks;
+    chunk /= p.row_blocks;
+  }
+  const int64_t a0 = __ldg(p.offsets + b), a1 = __ldg(p.offsets + b + 1);
+  const int j0 = chunk * p.jc;
+  const int j1 = min(p.H, j0 + p.jc);
+  const int spr = p.slots_per_row, R = p.rows_per_step;
+  const int r0 = div_magic(tid, p.spr_magic);
+  const int k = tid - r0 * spr;
+  const int wr0 = div_magic(warp * 32, p.spr_magic), wr1 = div_magic(warp * 32 + 31, p.spr_magic);
+  const int row_base = rblk * M * R;
+  const int row_end = min(p.W, row_base + M * R);
+
+  int64_t pos = a0;
+  const int n = build_list(p.supp, sh, pos, a1, c, j0, j1, row_base, row_end);
+  int nz = 0;
+  if (pos < a1 || n > p.stage_cap) {
+    nz = slab_rows_unstaged<M, VEC>(p, sh, b, c, a0, a1, j0, j1, row_base, row_end, r0, k, wr0,
+                                    wr1);
+  } else {
+    // Stage every candidate's gy (chunk rows), gx and gz rows in shared memory.
+    for (int q = warp; q < n; q += nw) {
+      const int64_t a = sh.meta[q].w;
+      float* dst = stage + q * p.stage_stride;
+      for (int e = lane; e < j1 - j0; e += 32) dst[e] = __ldg(p.ty + a * p.ry + j0 + e);
+      for (int e = lane; e < p.W; e += 32) dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + e);
+      const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz);
+      float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
+      for (int e = lane; e < (p.rz >> 2); e += 32) dst4[e] = __ldg(src4 + e);
+    }
+    // Warp-private ordered sublists: for each row step m, the candidates whose
+    // x-support meets this warp's rows, as {shared byte address of the staged
+    // block, slab mask over the chunk}.
+    const unsigned stage_s = (unsigned)__cvta_generic_to_shared(stage);
+    int2* lists = reinterpret_cast<int2*>(stage + p.stage_floats) + warp * M * p.stage_cap;
+    const unsigned lists_s = (unsigned)__cvta_generic_to_shared(lists);
+    int cnt[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int rlo = row_base + wr0 + m * R, rhi = row_base + wr1 + m * R;
+      int filled = 0;
+      for (int q0 = 0; q0 < n; q0 += 32) {
+        const int q = q0 + lane;
+        bool hit = false;
+        int2 ent = make_int2(0, 0);
+        if (q < n) {
+          const int4 s = sh.meta[q];
+          hit = lo16(s.x) <= rhi && hi16(s.x) > rlo;
+          const int lo = max(lo16(s.y), j0) - j0, hi = min(hi16(s.y), j1) - j0;
+          const unsigned long long mask = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
+          ent = make_int2((int)(stage_s + 4u * (unsigned)(q * p.stage_stride)), (int)(unsigned)mask);
+        }
+        const unsigned bal = __ballot_sync(kFull, hit);
+        if (hit) lists[m * p.stage_cap + filled + __popc(bal & ((1u << lane) - 1u))] = ent;
+        filled += __popc(bal);
+      }
+      cnt[m] = filled;
+    }
+    __syncthreads();  // staged tables visible to every warp (lists are warp-private)
+
+    Slot* out_c = reinterpret_cast<Slot*>(p.out + ((b * p.C + c) * (int64_t)p.H + j0) * p.slab_elems);
+    const int64_t slab_slots = p.slab_elems / (VEC ? 4 : 1);
+    const int ibase = row_base + r0;
+    const unsigned gz_off = 4u * (unsigned)(VEC ? p.stage_gz + 4 * k : p.stage_gz + k);
+    const unsigned gx_off = 4u * (unsigned)(p.stage_gx + ibase);
+    const int slot0 = ibase * spr + k;   // this thread's slot in the slab at step 0
+    const int slot_step = R * spr;       // = blockDim.x
+    for (int jj = 0; jj < j1 - j0; ++jj) {
+      const int jbit = 1 << jj;
+      const unsigned gy_off = 4u * (unsigned)jj;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        Slot acc;
+        zero_slot(acc);
+        const unsigned L = lists_s + 8u * (unsigned)(m * p.stage_cap);
+        const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
+#pragma unroll 1
+        for (int e = 0; e < cnt[m]; ++e) {
+          const int2 ent = lds_int2(L + 8u * (unsigned)e);  // ascending candidate order
+          if (!(ent.y & jbit)) continue;                      // uniform: y-support
+          const unsigned blk = (unsigned)ent.x;
+          Slot gz;
+          lds_slot(gz, blk + gz_off);
+          const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
+          add_scaled(acc, pyx, gz);                                              // (..) (x) tz, +=
+        }
+        if (ibase + m * R < row_end) {
+          out_c[jj * slab_slots + slot0 + m * slot_step] = acc;
+          if (cnt[m] != 0) nz += nonzeros_pos(acc);
+        }
+      }
+    }
+  }
+  if (p.stats != nullptr) finish_stats(p, sh, b, a0, a1, nz, c == 0 && chunk == 0 && rblk == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -524,34 +762,58 @@ VG_API int vg_axis_tables_f32(const vg_batch_desc* desc, void* workspace, size_t
 namespace {
 
 // K3 launch (tables must already be in the workspace, same stream).
+int gcd_int(int a, int b) { return b == 0 ? a : gcd_int(b, a % b); }
+
+// Launch shape of the row-structured kernel: NT = R * spr threads (a multiple
+// of 32), M <= 8 row steps per CTA, row_blocks CTAs per slab; minimises idle
+// rows, then prefers NT close to 256. False if no shape exists (huge rows).
+bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
+  const int base = spr / gcd_int(32, spr) * 32;  // lcm(32, spr)
+  if (base > kRowThreads) return false;
+  double best = 1e30;
+  for (int q = 1; base * q <= kRowThreads; ++q) {
+    const int t = base * q, r = t / spr;
+    const int need = (W + r - 1) / r;
+    const int m = need < 8 ? need : 8;
+    const int rb = (need + m - 1) / m;
+    const double waste = (double)(rb * m * r - W) / (rb * m * r);
+    const double score = waste + (t < 128 ? 0.25 : 0.0) + fabs(t - 256.0) * 1e-5;
+    if (score < best) {
+      best = score;
+      *nt = t;
+      *R = r;
+      *M = m;
+      *row_blocks = rb;
+    }
+  }
+  return true;
+}
+
+template <bool VEC>
+void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
+  switch (M) {
+    case 1: vg_slab_kernel<1, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 2: vg_slab_kernel<2, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 3: vg_slab_kernel<3, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 4: vg_slab_kernel<4, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 5: vg_slab_kernel<5, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 6: vg_slab_kernel<6, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 7: vg_slab_kernel<7, VEC><<<grid, nt, smem, st>>>(p); break;
+    default: vg_slab_kernel<8, VEC><<<grid, nt, smem, st>>>(p); break;
+  }
+}
+
+// K3 launch (tables must already be in the workspace, same stream).
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
                  vg_mol_stats* stats, cudaStream_t st) {
   const bool vec = (d.D % 4) == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   const int64_t slab = (int64_t)d.W * d.D;
   const int width = vec ? 4 : 1;
-  const int64_t nslots64 = slab / width;
-  if (nslots64 > INT_MAX / 2) return set_error(VG_ERR_INVALID, "slab W*D too large");
-  const int nslots = (int)nslots64;
-  // threads per CTA and slot steps per thread: NT <= 256, M <= 16, then
-  // split huge slabs into several CTAs (slot blocks)
-  int m_steps = 1;
-  while (m_steps < 16 && (nslots + m_steps - 1) / m_steps > kMaxThreads) m_steps *= 2;
-  int nt = (nslots + m_steps - 1) / m_steps;
-  nt = nt > kMaxThreads ? kMaxThreads : ((nt + 31) / 32) * 32;
-  const int per_block = nt * m_steps;
-  const int slot_blocks = (nslots + per_block - 1) / per_block;
-  // y-slabs per task: aim for >= 64 KiB of output per CTA
-  const int64_t bytes_per_slab_task = (int64_t)per_block * width * 4;
-  int jc = (int)((65536 + bytes_per_slab_task - 1) / bytes_per_slab_task);
-  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
-  const int n_jchunks = (d.H + jc - 1) / jc;
-  const int64_t tasks = d.n_molecules * d.C * (int64_t)n_jchunks * slot_blocks;
-  if (tasks > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)tasks);
+  const int spr = vec ? d.D / 4 : d.D;
+  const char* force = getenv("VG_FORCE_GENERIC");
+  int nt = 0, R = 0, M = 0, row_blocks = 0;
+  const bool rows_ok = !(force && force[0] == '1') && plan_rows(spr, d.W, &nt, &R, &M, &row_blocks);
 
-  if (stats != nullptr) {
-    cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * d.n_molecules, st);
-    if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
-  }
   SlabParams p;
   memset(&p, 0, sizeof p);
   p.offsets = d.offsets;
@@ -566,17 +828,70 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.ry = L.row_y;
   p.rz = L.row_z;
   p.H = d.H;
+  p.W = d.W;
   p.C = d.C;
+  p.slots_per_row = spr;
+
+  int64_t cta_bytes_per_slab;
+  int64_t blocks_per_slab;
+  if (rows_ok) {
+    cta_bytes_per_slab = (int64_t)(M * R < d.W ? M * R : d.W) * d.D * 4;
+    blocks_per_slab = row_blocks;
+  } else {
+    const int64_t nslots64 = slab / width;
+    if (nslots64 > INT_MAX / 2) return set_error(VG_ERR_INVALID, "slab W*D too large");
+    const int nslots = (int)nslots64;
+    int m_steps = 1;
+    while (m_steps < 16 && (nslots + m_steps - 1) / m_steps > 256) m_steps *= 2;
+    nt = (nslots + m_steps - 1) / m_steps;
+    nt = nt > 256 ? 256 : ((nt + 31) / 32) * 32;
+    const int per_block = nt * m_steps;
+    p.slot_blocks = (nslots + per_block - 1) / per_block;
+    p.nslots = nslots;
+    p.m_steps = m_steps;
+    cta_bytes_per_slab = (int64_t)per_block * width * 4;
+    blocks_per_slab = p.slot_blocks;
+  }
+  // y-slabs per task: aim for >= kTaskBytes of output per CTA (<= 32: slab masks)
+  int jc = (int)((kTaskBytes + cta_bytes_per_slab - 1) / cta_bytes_per_slab);
+  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
+  if (jc > 32) jc = 32;
   p.jc = jc;
-  p.n_jchunks = n_jchunks;
-  p.slot_blocks = slot_blocks;
-  p.nslots = nslots;
-  p.slots_per_row = vec ? d.D / 4 : d.D;
-  p.m_steps = m_steps;
+  p.n_jchunks = (d.H + jc - 1) / jc;
+  const int64_t tasks = d.n_molecules * d.C * (int64_t)p.n_jchunks * blocks_per_slab;
+  if (tasks > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)tasks);
+
+  if (stats != nullptr) {
+    cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * d.n_molecules, st);
+    if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
+  }
+  if (!rows_ok) {
+    if (vec)
+      vg_slab_generic_kernel<true><<<(unsigned)tasks, nt, 0, st>>>(p);
+    else
+      vg_slab_generic_kernel<false><<<(unsigned)tasks, nt, 0, st>>>(p);
+    return check_launch("vg_slab_generic_kernel");
+  }
+  if (d.C > 65535 || (int64_t)p.n_jchunks * row_blocks > 65535 || d.n_molecules > INT_MAX)
+    return set_error(VG_ERR_INVALID, "grid too large for the slab kernel");
+  p.row_blocks = row_blocks;
+  p.rows_per_step = R;
+  p.spr_magic = (0x100000000ull / (unsigned long long)spr) + 1ull;
+  p.stage_gx = (jc + 3) & ~3;
+  p.stage_gz = p.stage_gx + round_up4(d.W);
+  p.stage_stride = p.stage_gz + round_up4(d.D);
+  int cap = kStageBytes / (4 * p.stage_stride);
+  p.stage_cap = cap > 64 ? 64 : cap;
+  // slack: rows >= W of the last step read (and discard) past the last block;
+  // then the warp-private sublists (int2 per candidate, row step and warp)
+  p.stage_floats = (p.stage_cap * p.stage_stride + M * R + 8 + 3) & ~3;
+  const size_t smem = (size_t)p.stage_floats * sizeof(float) +
+                      (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
+  const dim3 grid((unsigned)d.n_molecules, (unsigned)d.C, (unsigned)(p.n_jchunks * row_blocks));
   if (vec)
-    vg_slab_kernel<true><<<(unsigned)tasks, nt, 0, st>>>(p);
+    launch_rows<true>(M, grid, nt, smem, st, p);
   else
-    vg_slab_kernel<false><<<(unsigned)tasks, nt, 0, st>>>(p);
+    launch_rows<false>(M, grid, nt, smem, st, p);
   return check_launch("vg_slab_kernel");
 }
 

@@ -350,3 +350,19 @@ def test_out_tensor_and_stream():
     s.synchronize()
     ref, _ = orc.batch(pb.offsets, pb.channels, pb.xyz, geom_of(cfg))
     assert_bitwise(out.cpu().numpy(), ref, "out=")
+
+
+def test_generic_kernel_matches_golden(monkeypatch):
+    """The fallback slab kernel (any shape, VG_FORCE_GENERIC=1) stays bit-exact."""
+    monkeypatch.setenv("VG_FORCE_GENERIC", "1")
+    for m, g in grid_cases():
+        lattice = vg.LatticeCell(tuple(m["periodic"])) if m["periodic"] else None
+        spec = vg.GridSpec(tuple(m["shape"]), m["channels"],
+                           vg.BoundingBox(tuple(m["origin"]), tuple(m["extents"])), m["sigma"],
+                           lattice)
+        ps = vg.ParticleSet(np.array(m["chans"], dtype=np.int64),
+                            np.array(m["pos"]).reshape(-1, 3), lattice)
+        grid, st = vg.generate_grid(ps, spec, mode=m["mode"], threshold=m["threshold"])
+        assert_bitwise(grid.numpy(), g, m["name"])
+        assert st.nonzero_voxels == m["nonzero_voxels"]
+    _compare_with_oracle(synth.CONFIGS[1], range(64))
