@@ -138,17 +138,24 @@ def dist_env():
 
 
 class Dist:
-    def __init__(self, world, rank, local):
+    """Barrier + max/sum over ranks (timing plumbing only; no data-path
+    collective). NCCL on GPUs; gloo on CPU for the multi-process tests."""
+
+    def __init__(self, world, rank, local, backend="nccl"):
         import torch
 
         self.world, self.rank, self.local = world, rank, local
         self.torch = torch
         self.pg = None
+        self.device = "cuda" if backend == "nccl" else "cpu"
         if world > 1:
             import torch.distributed as td
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if backend == "nccl":
+                td.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                td.init_process_group(backend, rank=rank, world_size=world)
             self.td = td
             self.pg = True
 
@@ -159,14 +166,14 @@ class Dist:
     def max(self, v: float) -> float:
         if not self.pg:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.device)
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return float(t.item())
 
     def sum(self, v: float) -> float:
         if not self.pg:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.device)
         self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
         return float(t.item())
 
@@ -178,8 +185,8 @@ class Dist:
 # ---------------------------------------------------------------------------
 # CPU: the reference algorithm (oracle port) on this host's cores
 # ---------------------------------------------------------------------------
-def cpu_rate(cfg, seconds: float, workers: int):
-    """grids/s of the oracle port over a bounded sample of ``cfg``."""
+def _cpu_sample(cfg, seconds: float, workers: int):
+    """Sample size for ~``seconds`` of work on ``workers`` cores (probe 8 grids)."""
     from oracle import voxgrid_oracle as orc
     from paper_2211_08506_b200 import synth
 
@@ -188,11 +195,26 @@ def cpu_rate(cfg, seconds: float, workers: int):
     t0 = time.perf_counter()
     orc.batch(probe.offsets, probe.channels, probe.xyz, geom, workers=1)
     per_grid = (time.perf_counter() - t0) / 8
-    n = int(min(cfg.n_molecules * 4, max(workers * 4, seconds * workers / max(per_grid, 1e-6))))
+    n = int(max(workers * 2, min(cfg.n_molecules * 4, seconds * workers / max(per_grid, 1e-6))))
+    return geom, n
+
+
+def cpu_rate(cfg, seconds: float, workers: int):
+    """grids/s of the oracle port (the reference algorithm, numpy) over a
+    bounded sample of ``cfg``, process pool writing into shared memory."""
+    from oracle import voxgrid_oracle as orc
+    from paper_2211_08506_b200 import synth
+
+    geom, n = _cpu_sample(cfg, seconds, workers)
     pb = synth.packed_batch(cfg, range(n))
-    t0 = time.perf_counter()
-    orc.batch(pb.offsets, pb.channels, pb.xyz, geom, workers=workers)
-    dt = time.perf_counter() - t0
+    pool = orc.Pool(geom, n, workers)
+    try:
+        pool.run(pb.offsets[:9] - 0, pb.channels, pb.xyz)  # warm the workers
+        t0 = time.perf_counter()
+        pool.run(pb.offsets, pb.channels, pb.xyz)
+        dt = time.perf_counter() - t0
+    finally:
+        pool.close()
     return n / dt, n, dt
 
 
@@ -205,30 +227,22 @@ def run_reference(args):
 
     cfg = synth.CONFIGS[args.config]
     workers = orc.host_cores()
-    geom = orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents, cfg.sigma)
-    # bounded per-step sample: ~2-3 s of work on all cores
-    probe = synth.packed_batch(cfg, range(8))
-    t0 = time.perf_counter()
-    orc.batch(probe.offsets, probe.channels, probe.xyz, geom, workers=1)
-    per_grid = (time.perf_counter() - t0) / 8
-    n = int(max(workers * 2, min(cfg.n_molecules, 2.5 * workers / max(per_grid, 1e-6))))
+    geom, n = _cpu_sample(cfg, 2.5, workers)   # ~2.5 s of CPU work per step
     pb = synth.packed_batch(cfg, range(n))
-    from concurrent.futures import ProcessPoolExecutor
-
-    jobs = [(pb.channels[pb.offsets[b]:pb.offsets[b + 1]], pb.xyz[pb.offsets[b]:pb.offsets[b + 1]],
-             geom, "sparse", None) for b in range(n)]
-    chunk = max(1, n // (workers * 4))
-    with ProcessPoolExecutor(max_workers=workers) as pool:
+    pool = orc.Pool(geom, n, workers)
+    try:
         for _ in range(args.warmup):
-            list(pool.map(orc._one, jobs, chunksize=chunk))
+            pool.run(pb.offsets, pb.channels, pb.xyz)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            list(pool.map(orc._one, jobs, chunksize=chunk))
+            pool.run(pb.offsets, pb.channels, pb.xyz)
         dt = time.perf_counter() - t0
+    finally:
+        pool.close()
     rate = n * args.steps / dt
     H, W, D = cfg.shape
     sample = (f"{n} molecules of {cfg.name} per step (numpy port of voxgrid.generate_grid, "
-              f"process pool of {workers})")
+              f"process pool of {workers} writing into shared memory)")
     line = {
         "impl": "reference", "metric": "grids_per_sec", "value": rate, "unit": "grids/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -426,7 +440,8 @@ def run_b200(args):
             line["cpu_baseline"] = {
                 "value": rate, "unit": "grids/s", "cores": workers, "kind": "port",
                 "sample": f"{n} molecules of {cfg.name} in {dt:.1f}s (numpy port of "
-                          f"voxgrid.generate_grid, process pool)"}
+                          f"voxgrid.generate_grid, process pool of {workers} writing into "
+                          f"shared memory)"}
         print(json.dumps(line), flush=True)
     return 0
 

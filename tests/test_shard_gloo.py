@@ -1,0 +1,78 @@
+"""Multi-GPU plumbing on CPU: molecule sharding (no collective on the data
+path) and bench.py's barrier / max-over-ranks timing, world_size 2 over gloo."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2211_08506_b200 import shard, synth
+
+
+def test_plan_shards_cover_and_balance():
+    rng = np.random.default_rng(0)
+    for world in (1, 2, 4, 8):
+        for n in (0, 1, 7, 64, 4096):
+            costs = rng.uniform(1, 10, n)
+            plan = shard.plan_shards(costs, world)
+            assert len(plan) == world
+            assert plan[0][0] == 0 and plan[-1][1] == n
+            for (a, b), (c, d) in zip(plan, plan[1:]):
+                assert b == c and a <= b
+            if n >= 64 * world:
+                per = [costs[a:b].sum() for a, b in plan]
+                assert max(per) - min(per) <= 2 * costs.max()
+    with pytest.raises(ValueError):
+        shard.plan_shards([1.0], 0)
+
+
+def test_cost_weighted_shards_for_skewed_config():
+    cfg = synth.CONFIGS[4]
+    pb = synth.packed_batch(cfg, range(512))
+    atoms = np.diff(pb.offsets)
+    costs = shard.molecule_costs(atoms, cfg.grid_bytes, bytes_per_atom=20_000.0)
+    plan = shard.plan_shards(costs, 8)
+    per = [costs[a:b].sum() for a, b in plan]
+    assert max(per) / min(per) < 1.05
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import bench
+
+    dist = bench.Dist(world, rank, rank, backend="gloo")
+    dist.barrier()
+    costs = np.arange(1, 101, dtype=float)
+    rng_ = shard.shard_range(100, rank, world, costs)
+    t_max = dist.max(float(rank + 1) * 1.5)
+    total = dist.sum(float(len(rng_)))
+    dist.close()
+    q.put((rank, rng_.start, rng_.stop, t_max, total))
+
+
+def test_gloo_world2_shards_and_max_over_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, a0, b0, m0, s0), (r1, a1, b1, m1, s1) = res
+    assert (a0, b1) == (0, 100) and b0 == a1           # disjoint, complete cover
+    assert m0 == m1 == 3.0                               # max over ranks
+    assert s0 == s1 == 100.0
