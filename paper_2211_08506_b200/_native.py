@@ -16,7 +16,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 INCLUDE = REPO_DIR / "include"
-LIB_PATH = PKG_DIR / "libvoxgrid_b200.so"
+LIB_PATH = Path(os.environ.get("VG_LIB", PKG_DIR / "libvoxgrid_b200.so"))  # VG_LIB: A/B builds
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",

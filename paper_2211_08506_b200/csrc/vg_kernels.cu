@@ -59,7 +59,11 @@ constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
 constexpr int kListCap = 256;        // K3: candidate segment capacity
 constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
 constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bound)
+#ifndef VG_ROW_MINB
+#define VG_ROW_MINB 4   // K3 row kernel: resident CTAs per SM the register budget targets
+#endif
 constexpr int kStageBytes = 16384;
+constexpr int kStageCapMax = 64;     // K3: staged candidates per sub-chunk (upper bound)
 constexpr int64_t kTaskBytes = 262144; // K3: output bytes per CTA (y-chunk sizing)   // K3: shared-memory staging budget per CTA
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
@@ -206,7 +210,7 @@ struct SlabParams {
   vg_mol_stats* stats;
   int64_t slab_elems;   // W*D
   int rx, ry, rz;       // table row strides
-  int H, W, C;
+  int H, W, D, C;
   int jc;               // y-slabs per task
   int n_jchunks;
   // generic kernel
@@ -218,7 +222,9 @@ struct SlabParams {
   // row-structured kernel
   int row_blocks;       // CTAs per slab along x rows
   int rows_per_step;    // R = blockDim.x / slots_per_row
-  unsigned long long spr_magic;  // floor(2^32 / slots_per_row) + 1
+  int zw;               // slots per row segment of one CTA (z window)
+  int z_blocks;         // CTAs per slab along z
+  unsigned long long zw_magic;   // floor(2^32 / zw) + 1
   int stage_cap;        // candidates that fit the shared-memory staging area
   int stage_stride;     // floats per staged candidate: gy[pad4(jc)] gx[pad4(W)] gz[pad4(D)]
   int stage_gx;         // offset of gx inside a staged block
@@ -241,7 +247,8 @@ __device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
 // x-support meets [xa, xb). Stops once at least kListCap entries are held;
 // `pos` returns the resume point.
 __device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t& pos, int64_t a1,
-                          int c, int jlo, int jhi, int xa, int xb) {
+                          int c, int jlo, int jhi, int xa, int xb, int za = 0,
+                          int zb = kMaxAxis) {
   const int nt = blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
   int count = 0;
@@ -252,7 +259,8 @@ __device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t
     if (idx < a1) {
       s = __ldg(supp + idx);
       keep = s.w == c && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
-             hi16(s.y) > jlo && lo16(s.x) < xb && hi16(s.x) > xa;
+             hi16(s.y) > jlo && lo16(s.x) < xb && hi16(s.x) > xa && lo16(s.z) < zb &&
+             hi16(s.z) > za;
     }
     const unsigned bal = __ballot_sync(kFull, keep);
     if (lane == 0) sh.warp_cnt[warp] = __popc(bal);
@@ -414,11 +422,14 @@ __global__ void __launch_bounds__(kMaxThreads) vg_slab_generic_kernel(const __gr
 }
 
 // --- row-structured kernel ----------------------------------------------------
-// Thread t owns slot k = t % spr of rows r0 + m*R (m < M, R = blockDim/spr):
-// no per-slot division, M accumulators in registers, candidates outer. A
-// warp's rows at step m are [wr0 + m*R, wr1 + m*R]; the warp skips a
-// candidate whose x-support misses them (uniform branch, exact: skipped terms
-// are +0). Grid = (molecule, channel, y-chunk x row-block).
+// A CTA owns a tile of y-slabs [j0, j1) x rows [row_base, row_end) x one z
+// window of zw slots (a slot = 4 z-contiguous voxels, or 1 on the scalar
+// path). Thread t owns slot k = zblk*zw + t % zw of rows r0 + m*R (m < M,
+// R = blockDim/zw): no per-slot division, one accumulator live. The y-chunk
+// is processed in sub-chunks halved until the candidate set fits shared
+// memory; each warp walks private ordered sublists of only the candidates
+// that meet its rows, so culling is exact (skipped terms are +0) and free.
+// Grid = (molecule, channel, y-chunk x row-block x z-block).
 
 __device__ __forceinline__ int div_magic(int n, unsigned long long magic) {
   return (int)(((unsigned long long)n * magic) >> 32);  // exact for n < 2^16, d < 2^16
@@ -433,15 +444,6 @@ __device__ __forceinline__ void add_scaled(float4& acc, float pyx, const float4&
 __device__ __forceinline__ void add_scaled(float& acc, float pyx, const float& gz) {
   acc = VG_FADD(acc, VG_FMUL(pyx, gz));
 }
-__device__ __forceinline__ void load_slot(float4& v, const float* row, int k) {
-  v = reinterpret_cast<const float4*>(row)[k];
-}
-__device__ __forceinline__ void load_slot(float& v, const float* row, int k) { v = row[k]; }
-__device__ __forceinline__ void ldg_slot(float4& v, const float* row, int k) {
-  v = __ldg(reinterpret_cast<const float4*>(row) + k);
-}
-__device__ __forceinline__ void ldg_slot(float& v, const float* row, int k) { v = __ldg(row + k); }
-
 // Explicit shared-space loads (32-bit addresses): keeps the hot loop free of
 // generic-to-shared address arithmetic.
 __device__ __forceinline__ float lds_f32(unsigned a) {
@@ -467,55 +469,63 @@ __device__ __forceinline__ int nonzeros_pos(const float4& a) {
 }
 __device__ __forceinline__ int nonzeros_pos(const float& a) { return min(__float_as_int(a), 1); }
 
-// Out-of-line path for chunks whose candidates do not fit the shared-memory
-// staging area (or exceed kListCap): tables are read through L1/L2 and the
-// list is rebuilt per slab in ascending segments. Returns the nonzero count.
-template <int M, bool VEC>
-__device__ __noinline__ int slab_rows_unstaged(const SlabParams& p, SlabShared& sh, int64_t b,
-                                               int c, int64_t a0, int64_t a1, int j0, int j1,
-                                               int row_base, int row_end, int r0, int k, int wr0,
-                                               int wr1) {
+// Per-CTA geometry shared by the staged and unstaged paths.
+struct RowTile {
+  int64_t b;
+  int c;
+  int64_t a0, a1;
+  int row_base, row_end;  // x rows of this CTA
+  int zv0, zv1;           // z voxels of this CTA's window
+  int r0, k;              // this thread's first row offset and global slot
+  int wr0, wr1;           // this warp's row offsets at step 0
+};
+
+// Hot loop of the row kernel for one staged segment: for each row step m
+// (unrolled) and slab j of the sub-chunk, walk the warp's ordered sublist,
+// accumulate fl32(acc + fl32(fl32(gy*gx)*gz)) and store the slot once.
+// FIRST=false continues sums stored by an earlier segment (own stores).
+// Returns the nonzero-count delta.
+template <int M>
+struct Counts {
+  int v[M];
+};
+
+template <int M, bool VEC, bool FIRST>
+__device__ __noinline__ int accumulate_rows(typename SlotT<VEC>::T* base, int64_t slab_slots,
+                                            int m_stride, int nj, int ibase, int row_end, int R,
+                                            Counts<M> cnt, unsigned lists_s, int cap,
+                                            unsigned gx_off, unsigned gz_off) {
   using Slot = typename SlotT<VEC>::T;
-  float* out_c = p.out + ((b * p.C + c) * (int64_t)p.H) * p.slab_elems;
-  const int R = p.rows_per_step, ibase = row_base + r0;
   int nz = 0;
-  for (int j = j0; j < j1; ++j) {
-    Slot acc[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) zero_slot(acc[m]);
-    unsigned touched = 0;
-    int64_t pos = a0;
-    while (pos < a1) {
-      __syncthreads();
-      const int n = build_list(p.supp, sh, pos, a1, c, j, j + 1, row_base, row_end);
-      for (int q = 0; q < n; ++q) {
-        const int4 s = sh.meta[q];
-        const int64_t a = s.w;
-        const float gy = __ldg(p.ty + a * p.ry + j);
-        const float* gx = p.tx + a * p.rx;
-        Slot gz;
-        ldg_slot(gz, p.tz + a * p.rz, k);
-        const int dlo = lo16(s.x) - (row_base + wr1);
-        const int dhi = hi16(s.x) - (row_base + wr0);
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          const int mr = m * R;
-          if (mr >= dlo && mr < dhi) {
-            const float pyx = VG_FMUL(gy, __ldg(gx + min(ibase + mr, p.W - 1)));
-            add_scaled(acc[m], pyx, gz);
-            touched |= 1u << m;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    float* slab = out_c + (int64_t)j * p.slab_elems;
+  Slot* dst_j = base;
+  for (int jj = 0; jj < nj; ++jj, dst_j += slab_slots) {
+    const int jbit = 1 << jj;
+    const unsigned gy_off = 4u * (unsigned)jj;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const int i = ibase + m * R;
-      if (i < row_end) {
-        store_slot(slab, i * p.slots_per_row + k, acc[m]);
-        if ((touched >> m) & 1u) nz += nonzeros(acc[m]);
+      const bool mine = ibase + m * R < row_end;
+      Slot* dst = dst_j + m * m_stride;
+      Slot acc;
+      zero_slot(acc);
+      if (!FIRST && mine) {
+        acc = *dst;
+        nz -= nonzeros_pos(acc);
+      }
+      const unsigned L = lists_s + 8u * (unsigned)(m * cap);
+      const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
+#pragma unroll 1
+      for (int e = 0; e < cnt.v[m]; ++e) {
+        const int2 ent = lds_int2(L + 8u * (unsigned)e);  // ascending candidate order
+        if (!(ent.y & jbit)) continue;                      // uniform: y-support
+        const unsigned blk = (unsigned)ent.x;
+        Slot gz;
+        lds_slot(gz, blk + gz_off);
+        const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
+        add_scaled(acc, pyx, gz);                                              // (..)(x)tz, +=
+      }
+      if (mine) {
+        *dst = acc;
+        if (!FIRST || cnt.v[m] != 0) nz += nonzeros_pos(acc);
       }
     }
   }
@@ -523,111 +533,132 @@ __device__ __noinline__ int slab_rows_unstaged(const SlabParams& p, SlabShared& 
 }
 
 template <int M, bool VEC>
-__global__ void __launch_bounds__(kRowThreads, 4) vg_slab_kernel(const __grid_constant__ SlabParams p) {
+__global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotT<VEC>::T;
+  constexpr int kWidth = VEC ? 4 : 1;
   __shared__ SlabShared sh;
   extern __shared__ float4 stage4[];
   float* stage = reinterpret_cast<float*>(stage4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
 
-  const int64_t b = blockIdx.x;
-  const int c = blockIdx.y;
-  int chunk = blockIdx.z, rblk = 0;
-  if (p.row_blocks > 1) {
-    rblk = chunk % p.row_blocks;
-    chunk /= p.row_blocks;
+  RowTile T;
+  T.b = blockIdx.x;
+  T.c = blockIdx.y;
+  int t = blockIdx.z, zblk = 0, rblk = 0;
+  if (p.z_blocks > 1) {
+    zblk = t % p.z_blocks;
+    t /= p.z_blocks;
   }
-  const int64_t a0 = __ldg(p.offsets + b), a1 = __ldg(p.offsets + b + 1);
+  if (p.row_blocks > 1) {
+    rblk = t % p.row_blocks;
+    t /= p.row_blocks;
+  }
+  const int chunk = t;
+  T.a0 = __ldg(p.offsets + T.b);
+  T.a1 = __ldg(p.offsets + T.b + 1);
   const int j0 = chunk * p.jc;
   const int j1 = min(p.H, j0 + p.jc);
-  const int spr = p.slots_per_row, R = p.rows_per_step;
-  const int r0 = div_magic(tid, p.spr_magic);
-  const int k = tid - r0 * spr;
-  const int wr0 = div_magic(warp * 32, p.spr_magic), wr1 = div_magic(warp * 32 + 31, p.spr_magic);
-  const int row_base = rblk * M * R;
-  const int row_end = min(p.W, row_base + M * R);
+  const int zw = p.zw, R = p.rows_per_step, spr = p.slots_per_row;
+  T.r0 = div_magic(tid, p.zw_magic);
+  T.k = zblk * zw + (tid - T.r0 * zw);
+  T.wr0 = div_magic(warp * 32, p.zw_magic);
+  T.wr1 = div_magic(warp * 32 + 31, p.zw_magic);
+  T.row_base = rblk * M * R;
+  T.row_end = min(p.W, T.row_base + M * R);
+  T.zv0 = zblk * zw * kWidth;
+  T.zv1 = min(p.D, T.zv0 + zw * kWidth);
 
-  int64_t pos = a0;
-  const int n = build_list(p.supp, sh, pos, a1, c, j0, j1, row_base, row_end);
+  const unsigned stage_s = (unsigned)__cvta_generic_to_shared(stage);
+  int2* lists = reinterpret_cast<int2*>(stage + p.stage_floats) + warp * M * p.stage_cap;
+  const unsigned lists_s = (unsigned)__cvta_generic_to_shared(lists);
+  const int ibase = T.row_base + T.r0;
+  const unsigned gz_off = 4u * (unsigned)(p.stage_gz + (T.k - zblk * zw) * kWidth);
+  const unsigned gx_off = 4u * (unsigned)(p.stage_gx + T.r0);
+  Slot* out_c = reinterpret_cast<Slot*>(p.out + (T.b * p.C + T.c) * (int64_t)p.H * p.slab_elems);
+  const int64_t slab_slots = p.slab_elems / kWidth;
+  const int slot0 = ibase * spr + T.k;
+
   int nz = 0;
-  if (pos < a1 || n > p.stage_cap) {
-    nz = slab_rows_unstaged<M, VEC>(p, sh, b, c, a0, a1, j0, j1, row_base, row_end, r0, k, wr0,
-                                    wr1);
-  } else {
-    // Stage every candidate's gy (chunk rows), gx and gz rows in shared memory.
-    for (int q = warp; q < n; q += nw) {
-      const int64_t a = sh.meta[q].w;
-      float* dst = stage + q * p.stage_stride;
-      for (int e = lane; e < j1 - j0; e += 32) dst[e] = __ldg(p.ty + a * p.ry + j0 + e);
-      for (int e = lane; e < p.W; e += 32) dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + e);
-      const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz);
-      float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
-      for (int e = lane; e < (p.rz >> 2); e += 32) dst4[e] = __ldg(src4 + e);
+  int js = j0, sc = j1 - j0;
+  while (js < j1) {
+    const int je = min(j1, js + sc);
+    int64_t pos = T.a0;
+    int n = build_list(p.supp, sh, pos, T.a1, T.c, js, je, T.row_base, T.row_end, T.zv0, T.zv1);
+    if ((pos < T.a1 || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
+      sc = (sc + 1) >> 1;
+      continue;
     }
-    // Warp-private ordered sublists: for each row step m, the candidates whose
-    // x-support meets this warp's rows, as {shared byte address of the staged
-    // block, slab mask over the chunk}.
-    const unsigned stage_s = (unsigned)__cvta_generic_to_shared(stage);
-    int2* lists = reinterpret_cast<int2*>(stage + p.stage_floats) + warp * M * p.stage_cap;
-    const unsigned lists_s = (unsigned)__cvta_generic_to_shared(lists);
-    int cnt[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const int rlo = row_base + wr0 + m * R, rhi = row_base + wr1 + m * R;
-      int filled = 0;
-      for (int q0 = 0; q0 < n; q0 += 32) {
-        const int q = q0 + lane;
-        bool hit = false;
-        int2 ent = make_int2(0, 0);
-        if (q < n) {
-          const int4 s = sh.meta[q];
-          hit = lo16(s.x) <= rhi && hi16(s.x) > rlo;
-          const int lo = max(lo16(s.y), j0) - j0, hi = min(hi16(s.y), j1) - j0;
-          const unsigned long long mask = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
-          ent = make_int2((int)(stage_s + 4u * (unsigned)(q * p.stage_stride)), (int)(unsigned)mask);
+    // Candidates are consumed in ascending segments of <= stage_cap. More than
+    // one segment only happens for a single over-dense slab: later segments
+    // continue the per-voxel sums from the values this thread already stored.
+    bool first = true;
+    for (;;) {
+      // n == 0 still runs one pass: every slot is stored (as zero) exactly once
+      for (int s0 = 0; s0 < max(n, 1); s0 += p.stage_cap) {
+        const int ns = min(p.stage_cap, n - s0);
+        const int4* meta = sh.meta + s0;
+        // Stage gy (sub-chunk rows), gx (CTA rows) and gz (z window) of each candidate.
+        const int rows = T.row_end - T.row_base;
+        for (int q = warp; q < ns; q += nw) {
+          const int64_t a = meta[q].w;
+          float* dst = stage + q * p.stage_stride;
+          for (int e = lane; e < je - js; e += 32) dst[e] = __ldg(p.ty + a * p.ry + js + e);
+          for (int e = lane; e < rows; e += 32)
+            dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + T.row_base + e);
+          if (VEC) {
+            const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz + T.zv0);
+            float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
+            for (int e = lane; e < zw; e += 32) dst4[e] = __ldg(src4 + e);
+          } else {
+            for (int e = lane; e < T.zv1 - T.zv0; e += 32)
+              dst[p.stage_gz + e] = __ldg(p.tz + a * p.rz + T.zv0 + e);
+          }
         }
-        const unsigned bal = __ballot_sync(kFull, hit);
-        if (hit) lists[m * p.stage_cap + filled + __popc(bal & ((1u << lane) - 1u))] = ent;
-        filled += __popc(bal);
-      }
-      cnt[m] = filled;
-    }
-    __syncthreads();  // staged tables visible to every warp (lists are warp-private)
+        // Warp-private ordered sublists: per row step m, the candidates whose
+        // x-support meets this warp's rows: {shared address of the block, slab mask}.
+        Counts<M> cnt;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int rlo = T.row_base + T.wr0 + m * R, rhi = T.row_base + T.wr1 + m * R;
+          int filled = 0;
+          for (int q0 = 0; q0 < ns; q0 += 32) {
+            const int q = q0 + lane;
+            bool hit = false;
+            int2 ent = make_int2(0, 0);
+            if (q < ns) {
+              const int4 s = meta[q];
+              hit = lo16(s.x) <= rhi && hi16(s.x) > rlo;
+              const int lo = max(lo16(s.y), js) - js, hi = min(hi16(s.y), je) - js;
+              const unsigned long long mask = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
+              ent = make_int2((int)(stage_s + 4u * (unsigned)(q * p.stage_stride)),
+                              (int)(unsigned)mask);
+            }
+            const unsigned bal = __ballot_sync(kFull, hit);
+            if (hit) lists[m * p.stage_cap + filled + __popc(bal & ((1u << lane) - 1u))] = ent;
+            filled += __popc(bal);
+          }
+          cnt.v[m] = filled;
+        }
+        __syncthreads();  // staged tables visible to every warp (lists are warp-private)
 
-    Slot* out_c = reinterpret_cast<Slot*>(p.out + ((b * p.C + c) * (int64_t)p.H + j0) * p.slab_elems);
-    const int64_t slab_slots = p.slab_elems / (VEC ? 4 : 1);
-    const int ibase = row_base + r0;
-    const unsigned gz_off = 4u * (unsigned)(VEC ? p.stage_gz + 4 * k : p.stage_gz + k);
-    const unsigned gx_off = 4u * (unsigned)(p.stage_gx + ibase);
-    const int slot0 = ibase * spr + k;   // this thread's slot in the slab at step 0
-    const int slot_step = R * spr;       // = blockDim.x
-    for (int jj = 0; jj < j1 - j0; ++jj) {
-      const int jbit = 1 << jj;
-      const unsigned gy_off = 4u * (unsigned)jj;
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        Slot acc;
-        zero_slot(acc);
-        const unsigned L = lists_s + 8u * (unsigned)(m * p.stage_cap);
-        const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
-#pragma unroll 1
-        for (int e = 0; e < cnt[m]; ++e) {
-          const int2 ent = lds_int2(L + 8u * (unsigned)e);  // ascending candidate order
-          if (!(ent.y & jbit)) continue;                      // uniform: y-support
-          const unsigned blk = (unsigned)ent.x;
-          Slot gz;
-          lds_slot(gz, blk + gz_off);
-          const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
-          add_scaled(acc, pyx, gz);                                              // (..) (x) tz, +=
-        }
-        if (ibase + m * R < row_end) {
-          out_c[jj * slab_slots + slot0 + m * slot_step] = acc;
-          if (cnt[m] != 0) nz += nonzeros_pos(acc);
-        }
+        if (first)
+          nz += accumulate_rows<M, VEC, true>(out_c + js * slab_slots + slot0, slab_slots,
+                                              R * spr, je - js, ibase, T.row_end, R, cnt, lists_s,
+                                              p.stage_cap, gx_off, gz_off);
+        else
+          nz += accumulate_rows<M, VEC, false>(out_c + js * slab_slots + slot0, slab_slots,
+                                               R * spr, je - js, ibase, T.row_end, R, cnt, lists_s,
+                                               p.stage_cap, gx_off, gz_off);
+        __syncthreads();  // the next segment / sub-chunk rewrites the staging area
+        first = false;
       }
+      if (pos >= T.a1) break;
+      n = build_list(p.supp, sh, pos, T.a1, T.c, js, je, T.row_base, T.row_end, T.zv0, T.zv1);
     }
+    js = je;
   }
-  if (p.stats != nullptr) finish_stats(p, sh, b, a0, a1, nz, c == 0 && chunk == 0 && rblk == 0);
+  if (p.stats != nullptr)
+    finish_stats(p, sh, T.b, T.a0, T.a1, nz, T.c == 0 && chunk == 0 && rblk == 0 && zblk == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -761,7 +792,6 @@ VG_API int vg_axis_tables_f32(const vg_batch_desc* desc, void* workspace, size_t
 
 namespace {
 
-// K3 launch (tables must already be in the workspace, same stream).
 int gcd_int(int a, int b) { return b == 0 ? a : gcd_int(b, a % b); }
 
 // Launch shape of the row-structured kernel: NT = R * spr threads (a multiple
@@ -803,6 +833,19 @@ void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const S
   }
 }
 
+// z window (slots per row segment) of the row kernel: whole rows up to 16
+// slots, 8-slot (32-float, 128 B) windows for wider rows so warps cull in z
+// too. VG_ZW overrides (tuning hook).
+int pick_zw(int spr) {
+  const char* env = getenv("VG_ZW");
+  if (env != nullptr) {
+    const int v = atoi(env);
+    if (v > 0 && spr % v == 0) return v;
+  }
+  if (spr > 16 && spr % 8 == 0) return 8;
+  return spr;
+}
+
 // K3 launch (tables must already be in the workspace, same stream).
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
                  vg_mol_stats* stats, cudaStream_t st) {
@@ -811,8 +854,9 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int width = vec ? 4 : 1;
   const int spr = vec ? d.D / 4 : d.D;
   const char* force = getenv("VG_FORCE_GENERIC");
+  const int zw = pick_zw(spr);
   int nt = 0, R = 0, M = 0, row_blocks = 0;
-  const bool rows_ok = !(force && force[0] == '1') && plan_rows(spr, d.W, &nt, &R, &M, &row_blocks);
+  const bool rows_ok = !(force && force[0] == '1') && plan_rows(zw, d.W, &nt, &R, &M, &row_blocks);
 
   SlabParams p;
   memset(&p, 0, sizeof p);
@@ -829,15 +873,16 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.rz = L.row_z;
   p.H = d.H;
   p.W = d.W;
+  p.D = d.D;
   p.C = d.C;
   p.slots_per_row = spr;
 
-  int64_t cta_bytes_per_slab;
-  int64_t blocks_per_slab;
-  if (rows_ok) {
-    cta_bytes_per_slab = (int64_t)(M * R < d.W ? M * R : d.W) * d.D * 4;
-    blocks_per_slab = row_blocks;
-  } else {
+  if (stats != nullptr) {
+    cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * d.n_molecules, st);
+    if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
+  }
+
+  if (!rows_ok) {
     const int64_t nslots64 = slab / width;
     if (nslots64 > INT_MAX / 2) return set_error(VG_ERR_INVALID, "slab W*D too large");
     const int nslots = (int)nslots64;
@@ -849,45 +894,49 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     p.slot_blocks = (nslots + per_block - 1) / per_block;
     p.nslots = nslots;
     p.m_steps = m_steps;
-    cta_bytes_per_slab = (int64_t)per_block * width * 4;
-    blocks_per_slab = p.slot_blocks;
-  }
-  // y-slabs per task: aim for >= kTaskBytes of output per CTA (<= 32: slab masks)
-  int jc = (int)((kTaskBytes + cta_bytes_per_slab - 1) / cta_bytes_per_slab);
-  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
-  if (jc > 32) jc = 32;
-  p.jc = jc;
-  p.n_jchunks = (d.H + jc - 1) / jc;
-  const int64_t tasks = d.n_molecules * d.C * (int64_t)p.n_jchunks * blocks_per_slab;
-  if (tasks > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)tasks);
-
-  if (stats != nullptr) {
-    cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * d.n_molecules, st);
-    if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
-  }
-  if (!rows_ok) {
+    const int64_t cta_bytes = (int64_t)per_block * width * 4;
+    int jc = (int)((kTaskBytes / 4 + cta_bytes - 1) / cta_bytes);
+    p.jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
+    p.n_jchunks = (d.H + p.jc - 1) / p.jc;
+    const int64_t tasks = d.n_molecules * d.C * (int64_t)p.n_jchunks * p.slot_blocks;
+    if (tasks > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)tasks);
     if (vec)
       vg_slab_generic_kernel<true><<<(unsigned)tasks, nt, 0, st>>>(p);
     else
       vg_slab_generic_kernel<false><<<(unsigned)tasks, nt, 0, st>>>(p);
     return check_launch("vg_slab_generic_kernel");
   }
-  if (d.C > 65535 || (int64_t)p.n_jchunks * row_blocks > 65535 || d.n_molecules > INT_MAX)
+
+  const int z_blocks = spr / zw;
+  const int rows_per_cta = M * R < d.W ? M * R : d.W;
+  const int64_t cta_bytes = (int64_t)rows_per_cta * zw * width * 4;
+  // y-slabs per CTA: aim for kTaskBytes of output (<= 32 for the slab masks)
+  int jc = (int)((kTaskBytes + cta_bytes - 1) / cta_bytes);
+  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
+  if (jc > 32) jc = 32;
+  p.jc = jc;
+  p.n_jchunks = (d.H + jc - 1) / jc;
+  if (d.C > 65535 || (int64_t)p.n_jchunks * row_blocks * z_blocks > 65535 ||
+      d.n_molecules > INT_MAX)
     return set_error(VG_ERR_INVALID, "grid too large for the slab kernel");
   p.row_blocks = row_blocks;
+  p.z_blocks = z_blocks;
+  p.zw = zw;
   p.rows_per_step = R;
-  p.spr_magic = (0x100000000ull / (unsigned long long)spr) + 1ull;
+  p.zw_magic = (0x100000000ull / (unsigned long long)zw) + 1ull;
+  // staged block per candidate: gy[pad4(jc)] gx[pad4(M*R)] gz[pad4(zw*width)]
   p.stage_gx = (jc + 3) & ~3;
-  p.stage_gz = p.stage_gx + round_up4(d.W);
-  p.stage_stride = p.stage_gz + round_up4(d.D);
+  p.stage_gz = p.stage_gx + round_up4(M * R);
+  p.stage_stride = p.stage_gz + round_up4(zw * width);
   int cap = kStageBytes / (4 * p.stage_stride);
-  p.stage_cap = cap > 64 ? 64 : cap;
+  p.stage_cap = cap > kStageCapMax ? kStageCapMax : cap;
   // slack: rows >= W of the last step read (and discard) past the last block;
   // then the warp-private sublists (int2 per candidate, row step and warp)
   p.stage_floats = (p.stage_cap * p.stage_stride + M * R + 8 + 3) & ~3;
   const size_t smem = (size_t)p.stage_floats * sizeof(float) +
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
-  const dim3 grid((unsigned)d.n_molecules, (unsigned)d.C, (unsigned)(p.n_jchunks * row_blocks));
+  const dim3 grid((unsigned)d.n_molecules, (unsigned)d.C,
+                  (unsigned)(p.n_jchunks * row_blocks * z_blocks));
   if (vec)
     launch_rows<true>(M, grid, nt, smem, st, p);
   else
