@@ -57,6 +57,8 @@ int check_launch(const char* what) {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
 constexpr int kListCap = 256;        // K3: candidate segment capacity
+constexpr int kC0Cap = 1536;         // K3 row kernel: level-0 candidates kept per CTA
+constexpr int kMaxCtaRows = 64;      // K3 row kernel: x rows per CTA (keeps staged rows short)
 constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
 constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bound)
 #ifndef VG_ROW_MINB
@@ -234,52 +236,100 @@ struct SlabParams {
 
 struct SlabShared {
   int4 meta[kListCap + kMaxThreads];  // {x supp, y supp, z supp, atom}
-  int warp_cnt[kMaxThreads / 32];
+  alignas(16) int warp_cnt[32];
+  int c0[kC0Cap];                     // row kernel: level-0 candidate atoms of the CTA
   long long red[kMaxThreads / 32];
 };
 
 __device__ __forceinline__ int lo16(int v) { return v & 0xffff; }
 __device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
 
-// Block-wide ordered compaction: scans atoms [pos, a1) in rounds of
-// blockDim.x and appends, in ascending atom order, every atom of channel c
-// with a non-empty support box whose y-support meets [jlo, jhi) and whose
-// x-support meets [xa, xb). Stops once at least kListCap entries are held;
-// `pos` returns the resume point.
-__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t& pos, int64_t a1,
-                          int c, int jlo, int jhi, int xa, int xb, int za = 0,
-                          int zb = kMaxAxis) {
-  const int nt = blockDim.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
+// Block-wide ordered compaction step: this thread's rank among the threads
+// of the block with keep == true (in thread order) and the block total.
+// Ends with the warp counts published; the caller must __syncthreads()
+// before the next call (warp_cnt is reused).
+__device__ __forceinline__ int block_rank(bool keep, int* warp_cnt, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned bal = __ballot_sync(kFull, keep);
+  if (lane == 0) warp_cnt[warp] = __popc(bal);
+  __syncthreads();
+  // all warp counts with 128-bit loads, then unrolled predicated sums (short
+  // latency chain: this sits between two barriers on every round)
+  const int4* c4 = reinterpret_cast<const int4*>(warp_cnt);
+  int before = 0;
+  total = 0;
+#pragma unroll
+  for (int g = 0; g < kMaxThreads / 128; ++g) {
+    if (g * 4 < nw) {
+      const int4 v = c4[g];
+      const int w0 = g * 4;
+      const int a = w0 + 0 < nw ? v.x : 0, b = w0 + 1 < nw ? v.y : 0;
+      const int c = w0 + 2 < nw ? v.z : 0, d = w0 + 3 < nw ? v.w : 0;
+      total += a + b + c + d;
+      before += (w0 + 0 < warp ? a : 0) + (w0 + 1 < warp ? b : 0) + (w0 + 2 < warp ? c : 0) +
+                (w0 + 3 < warp ? d : 0);
+    }
+  }
+  return before + __popc(bal & ((1u << lane) - 1u));
+}
+
+struct AtomFilter {
+  int c, jlo, jhi, xa, xb, za, zb;
+  __device__ __forceinline__ bool operator()(const int4& s) const {
+    return s.w == c && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
+           hi16(s.y) > jlo && lo16(s.x) < xb && hi16(s.x) > xa && lo16(s.z) < zb &&
+           hi16(s.z) > za;
+  }
+};
+
+// Ordered compaction into sh.meta: scans source positions [pos, end) in
+// rounds of blockDim.x (position p is atom src[p], or atom p when src is
+// NULL) and appends, in ascending atom order, every atom passing `f`. Stops
+// once at least kListCap entries are held; `pos` returns the resume point.
+__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, const int* src,
+                          int64_t& pos, int64_t end, const AtomFilter& f) {
   int count = 0;
-  while (pos < a1 && count < kListCap) {
-    const int64_t idx = pos + threadIdx.x;
+  while (pos < end && count < kListCap) {
+    const int64_t p = pos + threadIdx.x;
     bool keep = false;
     int4 s = make_int4(0, 0, 0, 0);
-    if (idx < a1) {
-      s = __ldg(supp + idx);
-      keep = s.w == c && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
-             hi16(s.y) > jlo && lo16(s.x) < xb && hi16(s.x) > xa && lo16(s.z) < zb &&
-             hi16(s.z) > za;
+    int64_t atom = 0;
+    if (p < end) {
+      atom = src != nullptr ? (int64_t)src[p] : p;
+      s = __ldg(supp + atom);
+      keep = f(s);
     }
-    const unsigned bal = __ballot_sync(kFull, keep);
-    if (lane == 0) sh.warp_cnt[warp] = __popc(bal);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int w = 0; w < nw; ++w) {
-      const int v = sh.warp_cnt[w];
-      before += (w < warp) ? v : 0;
-      total += v;
-    }
-    if (keep) {
-      const int rank = before + __popc(bal & ((1u << lane) - 1u));
-      sh.meta[count + rank] = make_int4(s.x, s.y, s.z, (int)idx);
-    }
+    int total;
+    const int rank = block_rank(keep, sh.warp_cnt, total);
+    if (keep) sh.meta[count + rank] = make_int4(s.x, s.y, s.z, (int)atom);
     count += total;
-    pos += nt;
+    pos += blockDim.x;
     __syncthreads();
   }
   return count;
+}
+
+__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t& pos, int64_t a1,
+                          int c, int jlo, int jhi, int xa, int xb) {
+  const AtomFilter f{c, jlo, jhi, xa, xb, 0, kMaxAxis};
+  return build_list(supp, sh, nullptr, pos, a1, f);
+}
+
+// Ordered compaction of atom indices into sh.c0 (the CTA's level-0
+// candidates). Returns the count, or -1 if more than kC0Cap atoms pass.
+__device__ int build_index_list(const int4* __restrict__ supp, SlabShared& sh, int64_t a0,
+                                int64_t a1, const AtomFilter& f) {
+  int count = 0;
+  for (int64_t pos = a0; pos < a1; pos += blockDim.x) {
+    const int64_t p = pos + threadIdx.x;
+    const bool keep = p < a1 && f(__ldg(supp + p));
+    int total;
+    const int rank = block_rank(keep, sh.warp_cnt, total);
+    if (keep && count + rank < kC0Cap) sh.c0[count + rank] = (int)p;
+    count += total;
+    __syncthreads();
+  }
+  return count <= kC0Cap ? count : -1;
 }
 
 template <bool VEC>
@@ -366,7 +416,7 @@ __device__ __forceinline__ void gather_slot(const SlabParams& p, const int4* met
 }
 
 template <bool VEC>
-__global__ void __launch_bounds__(kMaxThreads) vg_slab_generic_kernel(const __grid_constant__ SlabParams p) {
+__global__ void __launch_bounds__(256, 2) vg_slab_generic_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotT<VEC>::T;
   __shared__ SlabShared sh;
   const int nt = blockDim.x;
@@ -579,12 +629,21 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
   const int slot0 = ibase * spr + T.k;
 
   int nz = 0;
+  // Level 0: the CTA's candidates over its whole chunk, scanned once from the
+  // molecule's atoms; sub-chunk lists below filter this short list instead.
+  // (skipped for small molecules: scanning them directly is as cheap)
+  const AtomFilter f0{T.c, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
+  const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x ? build_index_list(p.supp, sh, T.a0, T.a1, f0)
+                                                        : -1;
+  const int* src = n0 >= 0 ? sh.c0 : nullptr;
+  const int64_t src_begin = n0 >= 0 ? 0 : T.a0, src_end = n0 >= 0 ? n0 : T.a1;
   int js = j0, sc = j1 - j0;
   while (js < j1) {
     const int je = min(j1, js + sc);
-    int64_t pos = T.a0;
-    int n = build_list(p.supp, sh, pos, T.a1, T.c, js, je, T.row_base, T.row_end, T.zv0, T.zv1);
-    if ((pos < T.a1 || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
+    const AtomFilter f{T.c, js, je, T.row_base, T.row_end, T.zv0, T.zv1};
+    int64_t pos = src_begin;
+    int n = build_list(p.supp, sh, src, pos, src_end, f);
+    if ((pos < src_end || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
       sc = (sc + 1) >> 1;
       continue;
     }
@@ -652,8 +711,8 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
         __syncthreads();  // the next segment / sub-chunk rewrites the staging area
         first = false;
       }
-      if (pos >= T.a1) break;
-      n = build_list(p.supp, sh, pos, T.a1, T.c, js, je, T.row_base, T.row_end, T.zv0, T.zv1);
+      if (pos >= src_end) break;
+      n = build_list(p.supp, sh, src, pos, src_end, f);
     }
     js = je;
   }
@@ -804,7 +863,9 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   for (int q = 1; base * q <= kRowThreads; ++q) {
     const int t = base * q, r = t / spr;
     const int need = (W + r - 1) / r;
-    const int m = need < 8 ? need : 8;
+    int m = need < 8 ? need : 8;
+    const int mcap = kMaxCtaRows / r > 1 ? kMaxCtaRows / r : 1;
+    if (m > mcap) m = mcap;
     const int rb = (need + m - 1) / m;
     const double waste = (double)(rb * m * r - W) / (rb * m * r);
     const double score = waste + (t < 128 ? 0.25 : 0.0) + fabs(t - 256.0) * 1e-5;
@@ -819,17 +880,32 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   return true;
 }
 
+template <int M, bool VEC>
+void launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
+  // The row kernel is register-limited to 4 CTAs/SM; ask for the largest
+  // shared-memory carveout so that shared memory never lowers that.
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(vg_slab_kernel<M, VEC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(vg_slab_kernel<M, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         96 * 1024);
+    configured = true;
+  }
+  vg_slab_kernel<M, VEC><<<grid, nt, smem, st>>>(p);
+}
+
 template <bool VEC>
 void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   switch (M) {
-    case 1: vg_slab_kernel<1, VEC><<<grid, nt, smem, st>>>(p); break;
-    case 2: vg_slab_kernel<2, VEC><<<grid, nt, smem, st>>>(p); break;
-    case 3: vg_slab_kernel<3, VEC><<<grid, nt, smem, st>>>(p); break;
-    case 4: vg_slab_kernel<4, VEC><<<grid, nt, smem, st>>>(p); break;
-    case 5: vg_slab_kernel<5, VEC><<<grid, nt, smem, st>>>(p); break;
-    case 6: vg_slab_kernel<6, VEC><<<grid, nt, smem, st>>>(p); break;
-    case 7: vg_slab_kernel<7, VEC><<<grid, nt, smem, st>>>(p); break;
-    default: vg_slab_kernel<8, VEC><<<grid, nt, smem, st>>>(p); break;
+    case 1: launch_rows_m<1, VEC>(grid, nt, smem, st, p); break;
+    case 2: launch_rows_m<2, VEC>(grid, nt, smem, st, p); break;
+    case 3: launch_rows_m<3, VEC>(grid, nt, smem, st, p); break;
+    case 4: launch_rows_m<4, VEC>(grid, nt, smem, st, p); break;
+    case 5: launch_rows_m<5, VEC>(grid, nt, smem, st, p); break;
+    case 6: launch_rows_m<6, VEC>(grid, nt, smem, st, p); break;
+    case 7: launch_rows_m<7, VEC>(grid, nt, smem, st, p); break;
+    default: launch_rows_m<8, VEC>(grid, nt, smem, st, p); break;
   }
 }
 

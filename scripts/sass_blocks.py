@@ -4,7 +4,8 @@ rep, top = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
-hdr, data = rows[1], rows[2:]
+hdr = rows[1]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r[0].startswith("0x")]
 ie, sc, ws = hdr.index("Instructions Executed"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
 tot = sum(float(r[ie] or 0) for r in data); st = sum(float(r[ws] or 0) for r in data) or 1
 blocks, cur = [], None
