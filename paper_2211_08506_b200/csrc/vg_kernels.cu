@@ -332,15 +332,27 @@ __device__ int build_index_list(const int4* __restrict__ supp, SlabShared& sh, i
   return count <= kC0Cap ? count : -1;
 }
 
+// A thread's slot: 1, 4 or 8 z-contiguous voxels (8 = two float4).
+struct Slot8 {
+  float4 a, b;
+};
+template <int SW>
+struct SlotW;
+template <>
+struct SlotW<1> { using T = float; };
+template <>
+struct SlotW<4> { using T = float4; };
+template <>
+struct SlotW<8> { using T = Slot8; };
 template <bool VEC>
-struct SlotT;
-template <>
-struct SlotT<true> { using T = float4; };
-template <>
-struct SlotT<false> { using T = float; };
+struct SlotT { using T = typename SlotW<VEC ? 4 : 1>::T; };
 
 __device__ __forceinline__ void zero_slot(float4& a) { a = make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ void zero_slot(float& a) { a = 0.f; }
+__device__ __forceinline__ void zero_slot(Slot8& a) {
+  zero_slot(a.a);
+  zero_slot(a.b);
+}
 __device__ __forceinline__ int nonzeros(const float4& a) {
   return (a.x != 0.f) + (a.y != 0.f) + (a.z != 0.f) + (a.w != 0.f);
 }
@@ -494,6 +506,10 @@ __device__ __forceinline__ void add_scaled(float4& acc, float pyx, const float4&
 __device__ __forceinline__ void add_scaled(float& acc, float pyx, const float& gz) {
   acc = VG_FADD(acc, VG_FMUL(pyx, gz));
 }
+__device__ __forceinline__ void add_scaled(Slot8& acc, float pyx, const Slot8& gz) {
+  add_scaled(acc.a, pyx, gz.a);
+  add_scaled(acc.b, pyx, gz.b);
+}
 // Explicit shared-space loads (32-bit addresses): keeps the hot loop free of
 // generic-to-shared address arithmetic.
 __device__ __forceinline__ float lds_f32(unsigned a) {
@@ -511,6 +527,10 @@ __device__ __forceinline__ void lds_slot(float4& v, unsigned a) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
 }
 __device__ __forceinline__ void lds_slot(float& v, unsigned a) { v = lds_f32(a); }
+__device__ __forceinline__ void lds_slot(Slot8& v, unsigned a) {
+  lds_slot(v.a, a);
+  lds_slot(v.b, a + 16u);
+}
 // Nonzero count of values known to be >= +0 (sums of products of masses):
 // such a float is nonzero iff its bit pattern is.
 __device__ __forceinline__ int nonzeros_pos(const float4& a) {
@@ -518,6 +538,9 @@ __device__ __forceinline__ int nonzeros_pos(const float4& a) {
          min(__float_as_int(a.w), 1);
 }
 __device__ __forceinline__ int nonzeros_pos(const float& a) { return min(__float_as_int(a), 1); }
+__device__ __forceinline__ int nonzeros_pos(const Slot8& a) {
+  return nonzeros_pos(a.a) + nonzeros_pos(a.b);
+}
 
 // Per-CTA geometry shared by the staged and unstaged paths.
 struct RowTile {
@@ -540,25 +563,51 @@ struct Counts {
   int v[M];
 };
 
-template <int M, bool VEC, bool FIRST>
-__device__ __noinline__ int accumulate_rows(typename SlotT<VEC>::T* base, int64_t slab_slots,
-                                            int m_stride, int nj, int ibase, int row_end, int R,
-                                            Counts<M> cnt, unsigned lists_s, int cap,
-                                            unsigned gx_off, unsigned gz_off) {
-  using Slot = typename SlotT<VEC>::T;
+// Slot I/O. SW=8 slots are two float4 half a z-window apart ("half" floats),
+// so that every 128-bit warp store still covers 512 contiguous bytes.
+__device__ __forceinline__ void st_slot(float* p, const float& v, int) { *p = v; }
+__device__ __forceinline__ void st_slot(float* p, const float4& v, int) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+__device__ __forceinline__ void st_slot(float* p, const Slot8& v, int half) {
+  *reinterpret_cast<float4*>(p) = v.a;
+  *reinterpret_cast<float4*>(p + half) = v.b;
+}
+__device__ __forceinline__ void ld_slot(float& v, const float* p, int) { v = *p; }
+__device__ __forceinline__ void ld_slot(float4& v, const float* p, int) {
+  v = *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void ld_slot(Slot8& v, const float* p, int half) {
+  v.a = *reinterpret_cast<const float4*>(p);
+  v.b = *reinterpret_cast<const float4*>(p + half);
+}
+__device__ __forceinline__ void lds_slot2(float& v, unsigned a, unsigned) { v = lds_f32(a); }
+__device__ __forceinline__ void lds_slot2(float4& v, unsigned a, unsigned) { lds_slot(v, a); }
+__device__ __forceinline__ void lds_slot2(Slot8& v, unsigned a, unsigned halfb) {
+  lds_slot(v.a, a);
+  lds_slot(v.b, a + halfb);
+}
+
+template <int M, int SW, bool FIRST>
+__device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int m_stride, int nj,
+                                            int ibase, int row_end, int R, Counts<M> cnt,
+                                            unsigned lists_s, int cap, unsigned gx_off,
+                                            unsigned gz_off, int half) {
+  using Slot = typename SlotW<SW>::T;
+  const unsigned halfb = 4u * (unsigned)half;
   int nz = 0;
-  Slot* dst_j = base;
-  for (int jj = 0; jj < nj; ++jj, dst_j += slab_slots) {
+  float* dst_j = base;
+  for (int jj = 0; jj < nj; ++jj, dst_j += slab_elems) {
     const int jbit = 1 << jj;
     const unsigned gy_off = 4u * (unsigned)jj;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const bool mine = ibase + m * R < row_end;
-      Slot* dst = dst_j + m * m_stride;
+      float* dst = dst_j + m * m_stride;
       Slot acc;
       zero_slot(acc);
       if (!FIRST && mine) {
-        acc = *dst;
+        ld_slot(acc, dst, half);
         nz -= nonzeros_pos(acc);
       }
       const unsigned L = lists_s + 8u * (unsigned)(m * cap);
@@ -569,12 +618,12 @@ __device__ __noinline__ int accumulate_rows(typename SlotT<VEC>::T* base, int64_
         if (!(ent.y & jbit)) continue;                      // uniform: y-support
         const unsigned blk = (unsigned)ent.x;
         Slot gz;
-        lds_slot(gz, blk + gz_off);
+        lds_slot2(gz, blk + gz_off, halfb);
         const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
         add_scaled(acc, pyx, gz);                                              // (..)(x)tz, +=
       }
       if (mine) {
-        *dst = acc;
+        st_slot(dst, acc, half);
         if (!FIRST || cnt.v[m] != 0) nz += nonzeros_pos(acc);
       }
     }
@@ -582,10 +631,10 @@ __device__ __noinline__ int accumulate_rows(typename SlotT<VEC>::T* base, int64_
   return nz;
 }
 
-template <int M, bool VEC>
+template <int M, int SW>
 __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const __grid_constant__ SlabParams p) {
-  using Slot = typename SlotT<VEC>::T;
-  constexpr int kWidth = VEC ? 4 : 1;
+  using Slot = typename SlotW<SW>::T;
+  constexpr int kWidth = SW;
   __shared__ SlabShared sh;
   extern __shared__ float4 stage4[];
   float* stage = reinterpret_cast<float*>(stage4);
@@ -622,11 +671,14 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
   int2* lists = reinterpret_cast<int2*>(stage + p.stage_floats) + warp * M * p.stage_cap;
   const unsigned lists_s = (unsigned)__cvta_generic_to_shared(lists);
   const int ibase = T.row_base + T.r0;
-  const unsigned gz_off = 4u * (unsigned)(p.stage_gz + (T.k - zblk * zw) * kWidth);
+  // this thread's first z (floats) in the row; SW=8 slots pair quads kk and kk + zw
+  const int kk = T.k - zblk * zw;
+  const int zf = T.zv0 + (SW == 8 ? 4 * kk : kk * kWidth);
+  const int half = SW == 8 ? 4 * zw : 0;
+  const unsigned gz_off = 4u * (unsigned)(p.stage_gz + (zf - T.zv0));
   const unsigned gx_off = 4u * (unsigned)(p.stage_gx + T.r0);
-  Slot* out_c = reinterpret_cast<Slot*>(p.out + (T.b * p.C + T.c) * (int64_t)p.H * p.slab_elems);
-  const int64_t slab_slots = p.slab_elems / kWidth;
-  const int slot0 = ibase * spr + T.k;
+  float* out_c = p.out + (T.b * p.C + T.c) * (int64_t)p.H * p.slab_elems;
+  const int slot0 = ibase * p.D + zf;  // float offset in the slab
 
   int nz = 0;
   // Level 0: the CTA's candidates over its whole chunk, scanned once from the
@@ -664,10 +716,10 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
           for (int e = lane; e < je - js; e += 32) dst[e] = __ldg(p.ty + a * p.ry + js + e);
           for (int e = lane; e < rows; e += 32)
             dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + T.row_base + e);
-          if (VEC) {
+          if (SW >= 4) {
             const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz + T.zv0);
             float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
-            for (int e = lane; e < zw; e += 32) dst4[e] = __ldg(src4 + e);
+            for (int e = lane; e < zw * (SW / 4); e += 32) dst4[e] = __ldg(src4 + e);
           } else {
             for (int e = lane; e < T.zv1 - T.zv0; e += 32)
               dst[p.stage_gz + e] = __ldg(p.tz + a * p.rz + T.zv0 + e);
@@ -701,13 +753,13 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
         __syncthreads();  // staged tables visible to every warp (lists are warp-private)
 
         if (first)
-          nz += accumulate_rows<M, VEC, true>(out_c + js * slab_slots + slot0, slab_slots,
-                                              R * spr, je - js, ibase, T.row_end, R, cnt, lists_s,
-                                              p.stage_cap, gx_off, gz_off);
+          nz += accumulate_rows<M, SW, true>(out_c + js * p.slab_elems + slot0, p.slab_elems,
+                                              R * p.D, je - js, ibase, T.row_end, R, cnt, lists_s,
+                                              p.stage_cap, gx_off, gz_off, half);
         else
-          nz += accumulate_rows<M, VEC, false>(out_c + js * slab_slots + slot0, slab_slots,
-                                               R * spr, je - js, ibase, T.row_end, R, cnt, lists_s,
-                                               p.stage_cap, gx_off, gz_off);
+          nz += accumulate_rows<M, SW, false>(out_c + js * p.slab_elems + slot0, p.slab_elems,
+                                               R * p.D, je - js, ibase, T.row_end, R, cnt, lists_s,
+                                               p.stage_cap, gx_off, gz_off, half);
         __syncthreads();  // the next segment / sub-chunk rewrites the staging area
         first = false;
       }
@@ -880,59 +932,76 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   return true;
 }
 
-template <int M, bool VEC>
+template <int M, int SW>
 void launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   // The row kernel is register-limited to 4 CTAs/SM; ask for the largest
   // shared-memory carveout so that shared memory never lowers that.
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(vg_slab_kernel<M, VEC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(vg_slab_kernel<M, SW>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(vg_slab_kernel<M, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(vg_slab_kernel<M, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          96 * 1024);
     configured = true;
   }
-  vg_slab_kernel<M, VEC><<<grid, nt, smem, st>>>(p);
+  vg_slab_kernel<M, SW><<<grid, nt, smem, st>>>(p);
 }
 
-template <bool VEC>
+template <int SW>
 void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   switch (M) {
-    case 1: launch_rows_m<1, VEC>(grid, nt, smem, st, p); break;
-    case 2: launch_rows_m<2, VEC>(grid, nt, smem, st, p); break;
-    case 3: launch_rows_m<3, VEC>(grid, nt, smem, st, p); break;
-    case 4: launch_rows_m<4, VEC>(grid, nt, smem, st, p); break;
-    case 5: launch_rows_m<5, VEC>(grid, nt, smem, st, p); break;
-    case 6: launch_rows_m<6, VEC>(grid, nt, smem, st, p); break;
-    case 7: launch_rows_m<7, VEC>(grid, nt, smem, st, p); break;
-    default: launch_rows_m<8, VEC>(grid, nt, smem, st, p); break;
+    case 1: launch_rows_m<1, SW>(grid, nt, smem, st, p); break;
+    case 2: launch_rows_m<2, SW>(grid, nt, smem, st, p); break;
+    case 3: launch_rows_m<3, SW>(grid, nt, smem, st, p); break;
+    case 4: launch_rows_m<4, SW>(grid, nt, smem, st, p); break;
+    case 5: launch_rows_m<5, SW>(grid, nt, smem, st, p); break;
+    case 6: launch_rows_m<6, SW>(grid, nt, smem, st, p); break;
+    case 7: launch_rows_m<7, SW>(grid, nt, smem, st, p); break;
+    default: launch_rows_m<8, SW>(grid, nt, smem, st, p); break;
   }
 }
 
 // z window (slots per row segment) of the row kernel: whole rows up to 16
 // slots, 8-slot (32-float, 128 B) windows for wider rows so warps cull in z
 // too. VG_ZW overrides (tuning hook).
-int pick_zw(int spr) {
+int pick_zw(int spr, int sw) {
   const char* env = getenv("VG_ZW");
   if (env != nullptr) {
     const int v = atoi(env);
     if (v > 0 && spr % v == 0) return v;
   }
-  if (spr > 16 && spr % 8 == 0) return 8;
+  const int win = 32 / sw;  // 32-float (128 B) windows on rows wider than 64 floats
+  if (spr * sw > 64 && win > 0 && spr % win == 0) return win;
   return spr;
+}
+
+// Slot width (voxels per thread slot): 8 (two float4, half a z-window
+// apart) when D % 8 == 0, else 4 (float4), else 1. VG_SW overrides.
+int pick_sw(int D, bool aligned16) {
+  int sw = !aligned16 || D % 4 != 0 ? 1 : (D % 8 == 0 ? 8 : 4);
+  const char* env = getenv("VG_SW");
+  if (env != nullptr) {
+    const int v = atoi(env);
+    if ((v == 1) || (v == 4 && aligned16 && D % 4 == 0) || (v == 8 && aligned16 && D % 8 == 0))
+      sw = v;
+  }
+  return sw;
 }
 
 // K3 launch (tables must already be in the workspace, same stream).
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
                  vg_mol_stats* stats, cudaStream_t st) {
-  const bool vec = (d.D % 4) == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  const bool aligned16 = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  const int sw = pick_sw(d.D, aligned16);
   const int64_t slab = (int64_t)d.W * d.D;
-  const int width = vec ? 4 : 1;
-  const int spr = vec ? d.D / 4 : d.D;
   const char* force = getenv("VG_FORCE_GENERIC");
-  const int zw = pick_zw(spr);
+  const int zw = pick_zw(d.D / sw, sw);
   int nt = 0, R = 0, M = 0, row_blocks = 0;
   const bool rows_ok = !(force && force[0] == '1') && plan_rows(zw, d.W, &nt, &R, &M, &row_blocks);
+  // the generic kernel works in float4 or float slots
+  const bool vec = rows_ok ? sw >= 4 : (d.D % 4 == 0 && aligned16);
+  const int width = rows_ok ? sw : (vec ? 4 : 1);
+  const int spr = d.D / width;
 
   SlabParams p;
   memset(&p, 0, sizeof p);
@@ -1013,10 +1082,12 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
   const dim3 grid((unsigned)d.n_molecules, (unsigned)d.C,
                   (unsigned)(p.n_jchunks * row_blocks * z_blocks));
-  if (vec)
-    launch_rows<true>(M, grid, nt, smem, st, p);
+  if (sw == 8)
+    launch_rows<8>(M, grid, nt, smem, st, p);
+  else if (sw == 4)
+    launch_rows<4>(M, grid, nt, smem, st, p);
   else
-    launch_rows<false>(M, grid, nt, smem, st, p);
+    launch_rows<1>(M, grid, nt, smem, st, p);
   return check_launch("vg_slab_kernel");
 }
 

@@ -366,3 +366,21 @@ def test_generic_kernel_matches_golden(monkeypatch):
         assert_bitwise(grid.numpy(), g, m["name"])
         assert st.nonzero_voxels == m["nonzero_voxels"]
     _compare_with_oracle(synth.CONFIGS[1], range(64))
+
+
+@pytest.mark.parametrize("sw", ["1", "4"])
+def test_slot_width_variants_match_golden(monkeypatch, sw):
+    """The row kernel's narrower slot layouts (VG_SW) stay bit-exact."""
+    monkeypatch.setenv("VG_SW", sw)
+    for m, g in grid_cases():
+        lattice = vg.LatticeCell(tuple(m["periodic"])) if m["periodic"] else None
+        spec = vg.GridSpec(tuple(m["shape"]), m["channels"],
+                           vg.BoundingBox(tuple(m["origin"]), tuple(m["extents"])), m["sigma"],
+                           lattice)
+        ps = vg.ParticleSet(np.array(m["chans"], dtype=np.int64),
+                            np.array(m["pos"]).reshape(-1, 3), lattice)
+        grid, st = vg.generate_grid(ps, spec, mode=m["mode"], threshold=m["threshold"])
+        assert_bitwise(grid.numpy(), g, m["name"])
+        assert st.nonzero_voxels == m["nonzero_voxels"]
+    _compare_with_oracle(synth.CONFIGS[4], range(0, 4096, 41))
+    _compare_with_oracle(synth.CONFIGS[3], [3])
