@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p)
 #pragma unroll
   for (int im = 0; im < 3; ++im) {
     e_cur[im] = 0.0f;
-    if (im < images && lane <= n) e_cur[im] = vg_erf_f32(vg_edge_arg(rel[im], d, lane, s));
+    if (im < images && lane <= n) e_cur[im] = vg_erf_sat_f32(vg_edge_arg(rel[im], d, lane, s));
   }
   int lo = -1, hi = 0;
   for (int c0 = 0; c0 < n; c0 += 32) {
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p)
 #pragma unroll
     for (int im = 0; im < 3; ++im) {
       e_nxt[im] = 0.0f;
-      if (im < images && e + 32 <= n) e_nxt[im] = vg_erf_f32(vg_edge_arg(rel[im], d, e + 32, s));
+      if (im < images && e + 32 <= n) e_nxt[im] = vg_erf_sat_f32(vg_edge_arg(rel[im], d, e + 32, s));
     }
     float g = 0.0f;
 #pragma unroll

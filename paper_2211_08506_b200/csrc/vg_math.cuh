@@ -119,6 +119,18 @@ VG_HD float vg_erf_f32(float t) {
   return (t > 0.0f) ? v : ((t < 0.0f) ? -v : VG_FMUL(0.0f, v));
 }
 
+// Saturation: for every float32 t >= VG_TSAT, vg_erf_f32(t) == 1.0f exactly
+// (and -1.0f for t <= -VG_TSAT, by odd symmetry); VG_TSAT is the successor of
+// the largest t with E(t) < 1 (exhaustive scan, tests/test_native_cpu.py).
+#define VG_TSAT 0x1.01a2a2p+2f
+
+// E(t) with the saturated tails answered without evaluating the series.
+VG_HD float vg_erf_sat_f32(float t) {
+  if (t >= VG_TSAT) return 1.0f;
+  if (t <= -VG_TSAT) return -1.0f;
+  return vg_erf_f32(t);
+}
+
 // ---- fp64 edge argument, kernels.py:252-254 (open) / :247-251 (periodic) ----
 // open axis:      t_e = fl32( ((o - mu) + delta*e) * s ),  rel = o - mu
 // periodic image: t_e = fl32( (-p + delta*e) * s ),        rel = -p

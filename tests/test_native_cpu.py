@@ -107,3 +107,18 @@ def test_invalid_descriptor_reports_error_without_gpu(lib):
     d.offsets = 8  # any non-NULL pointer; layout never dereferences it
     assert lib.vg_workspace_layout(ctypes.byref(d), ctypes.byref(layout)) == 0
     assert layout.total >= 256 and layout.row_x == 8
+
+
+def test_erf_saturation_threshold(lib):
+    """K1 skips the series where E(t) is exactly +-1: E(t) == 1.0f for every
+    float32 t >= t_sat (checked on every float in [t_sat, t_sat*4) and a
+    sample up to +inf), and E(prev(t_sat)) < 1."""
+    tsat = np.float32(float.fromhex("0x1.01a2a2p+2"))
+    below = np.nextafter(tsat, np.float32(0), dtype=np.float32)
+    lo = int(tsat.view(np.uint32))
+    dense = np.arange(lo, lo + (2 << 23), dtype=np.uint32).view(np.float32)
+    sparse = np.arange(lo, 0x7F800001, 9973, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    for t in (dense, sparse):
+        assert np.all(_host(lib.vg_erf_f32_host, t) == 1.0)
+        assert np.all(_host(lib.vg_erf_f32_host, -t) == -1.0)
+    assert _host(lib.vg_erf_f32_host, np.array([below], np.float32))[0] < 1.0
