@@ -56,16 +56,16 @@ int check_launch(const char* what) {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
-constexpr int kListCap = 256;        // K3: candidate segment capacity
-constexpr int kC0Cap = 1536;         // K3 row kernel: level-0 candidates kept per CTA
+constexpr int kListCap = 128;        // K3: candidate segment capacity (>= kStageCapMax)
+constexpr int kC0CapMax = 1536;      // K3 row kernel: level-0 candidates kept per CTA (max)
 constexpr int kMaxCtaRows = 64;      // K3 row kernel: x rows per CTA (keeps staged rows short)
 constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
 constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bound)
 #ifndef VG_ROW_MINB
 #define VG_ROW_MINB 4   // K3 row kernel: resident CTAs per SM the register budget targets
 #endif
-constexpr int kStageBytes = 16384;
-constexpr int kStageCapMax = 64;     // K3: staged candidates per sub-chunk (upper bound)
+constexpr int kStageBytes = 24576;
+constexpr int kStageCapMax = 96;     // K3: staged candidates per sub-chunk (upper bound)
 constexpr int64_t kTaskBytes = 262144; // K3: output bytes per CTA (y-chunk sizing)   // K3: shared-memory staging budget per CTA
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
@@ -232,12 +232,12 @@ struct SlabParams {
   int stage_gx;         // offset of gx inside a staged block
   int stage_gz;         // offset of gz inside a staged block
   int stage_floats;     // floats of the staging area (sublists follow it)
+  int c0_cap;           // level-0 candidate capacity (ints before the staging area)
 };
 
 struct SlabShared {
-  int4 meta[kListCap + kMaxThreads];  // {x supp, y supp, z supp, atom}
+  int4 meta[kListCap + 256];          // {x supp, y supp, z supp, atom}; blockDim <= 256
   alignas(16) int warp_cnt[32];
-  int c0[kC0Cap];                     // row kernel: level-0 candidate atoms of the CTA
   long long red[kMaxThreads / 32];
 };
 
@@ -315,21 +315,21 @@ __device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t
   return build_list(supp, sh, nullptr, pos, a1, f);
 }
 
-// Ordered compaction of atom indices into sh.c0 (the CTA's level-0
-// candidates). Returns the count, or -1 if more than kC0Cap atoms pass.
-__device__ int build_index_list(const int4* __restrict__ supp, SlabShared& sh, int64_t a0,
-                                int64_t a1, const AtomFilter& f) {
+// Ordered compaction of atom indices into c0 (the CTA's level-0
+// candidates). Returns the count, or -1 if more than cap atoms pass.
+__device__ int build_index_list(const int4* __restrict__ supp, SlabShared& sh, int* c0, int cap,
+                                int64_t a0, int64_t a1, const AtomFilter& f) {
   int count = 0;
   for (int64_t pos = a0; pos < a1; pos += blockDim.x) {
     const int64_t p = pos + threadIdx.x;
     const bool keep = p < a1 && f(__ldg(supp + p));
     int total;
     const int rank = block_rank(keep, sh.warp_cnt, total);
-    if (keep && count + rank < kC0Cap) sh.c0[count + rank] = (int)p;
+    if (keep && count + rank < cap) c0[count + rank] = (int)p;
     count += total;
     __syncthreads();
   }
-  return count <= kC0Cap ? count : -1;
+  return count <= cap ? count : -1;
 }
 
 // A thread's slot: 1, 4 or 8 z-contiguous voxels (8 = two float4).
@@ -612,15 +612,23 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
       }
       const unsigned L = lists_s + 8u * (unsigned)(m * cap);
       const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
-#pragma unroll 1
-      for (int e = 0; e < cnt.v[m]; ++e) {
-        const int2 ent = lds_int2(L + 8u * (unsigned)e);  // ascending candidate order
-        if (!(ent.y & jbit)) continue;                      // uniform: y-support
-        const unsigned blk = (unsigned)ent.x;
-        Slot gz;
-        lds_slot2(gz, blk + gz_off, halfb);
-        const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
-        add_scaled(acc, pyx, gz);                                              // (..)(x)tz, +=
+      // 32 entries at a time: each lane tests one entry's slab mask, the
+      // ballot gives the entries active on this slab, visited in ascending
+      // order (ascending atom order) with no cost for the inactive ones.
+      for (int c0 = 0; c0 < cnt.v[m]; c0 += 32) {
+        const int e = c0 + (int)(threadIdx.x & 31);
+        int2 mine_ent = make_int2(0, 0);
+        if (e < cnt.v[m]) mine_ent = lds_int2(L + 8u * (unsigned)e);
+        unsigned act = __ballot_sync(kFull, (mine_ent.y & jbit) != 0);
+        while (act != 0u) {
+          const int bit = __ffs(act) - 1;
+          act &= act - 1u;
+          const unsigned blk = (unsigned)__shfl_sync(kFull, mine_ent.x, bit);
+          Slot gz;
+          lds_slot2(gz, blk + gz_off, halfb);
+          const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
+          add_scaled(acc, pyx, gz);                                              // (..)(x)tz, +=
+        }
       }
       if (mine) {
         st_slot(dst, acc, half);
@@ -636,8 +644,9 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
   using Slot = typename SlotW<SW>::T;
   constexpr int kWidth = SW;
   __shared__ SlabShared sh;
-  extern __shared__ float4 stage4[];
-  float* stage = reinterpret_cast<float*>(stage4);
+  extern __shared__ float4 dyn4[];
+  int* c0 = reinterpret_cast<int*>(dyn4);             // level-0 candidates [c0_cap]
+  float* stage = reinterpret_cast<float*>(dyn4) + p.c0_cap;  // staged tables, then sublists
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
 
   RowTile T;
@@ -685,9 +694,10 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
   // molecule's atoms; sub-chunk lists below filter this short list instead.
   // (skipped for small molecules: scanning them directly is as cheap)
   const AtomFilter f0{T.c, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
-  const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x ? build_index_list(p.supp, sh, T.a0, T.a1, f0)
-                                                        : -1;
-  const int* src = n0 >= 0 ? sh.c0 : nullptr;
+  const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x && p.c0_cap > 0
+                     ? build_index_list(p.supp, sh, c0, p.c0_cap, T.a0, T.a1, f0)
+                     : -1;
+  const int* src = n0 >= 0 ? c0 : nullptr;
   const int64_t src_begin = n0 >= 0 ? 0 : T.a0, src_end = n0 >= 0 ? n0 : T.a1;
   int js = j0, sc = j1 - j0;
   while (js < j1) {
@@ -1073,12 +1083,20 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.stage_gx = (jc + 3) & ~3;
   p.stage_gz = p.stage_gx + round_up4(M * R);
   p.stage_stride = p.stage_gz + round_up4(zw * width);
+  // staging capacity: what the batch's molecules need (about 2x the mean atom
+  // count), within the byte budget; small molecules keep CTAs small
+  const int64_t mean_atoms = d.n_molecules > 0 ? (d.n_atoms + d.n_molecules - 1) / d.n_molecules : 0;
   int cap = kStageBytes / (4 * p.stage_stride);
-  p.stage_cap = cap > kStageCapMax ? kStageCapMax : cap;
+  const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > kStageCapMax ? kStageCapMax : mean_atoms * 2));
+  if (cap > want) cap = want;
+  p.stage_cap = cap < 1 ? 1 : cap;
+  // level-0 list only pays for large molecules (it is used when a molecule
+  // has more than 2*blockDim atoms); capacity in ints, 16-byte aligned
+  p.c0_cap = mean_atoms > 64 ? kC0CapMax : 256;
   // slack: rows >= W of the last step read (and discard) past the last block;
   // then the warp-private sublists (int2 per candidate, row step and warp)
   p.stage_floats = (p.stage_cap * p.stage_stride + M * R + 8 + 3) & ~3;
-  const size_t smem = (size_t)p.stage_floats * sizeof(float) +
+  const size_t smem = (size_t)p.c0_cap * sizeof(int) + (size_t)p.stage_floats * sizeof(float) +
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
   const dim3 grid((unsigned)d.n_molecules, (unsigned)d.C,
                   (unsigned)(p.n_jchunks * row_blocks * z_blocks));
