@@ -384,3 +384,32 @@ def test_slot_width_variants_match_golden(monkeypatch, sw):
         assert st.nonzero_voxels == m["nonzero_voxels"]
     _compare_with_oracle(synth.CONFIGS[4], range(0, 4096, 41))
     _compare_with_oracle(synth.CONFIGS[3], [3])
+
+
+def test_pipeline_matches_serial_path():
+    """GridPipeline (copy / tables / compute streams, double buffers) gives
+    the serial path's bits for host and device inputs, across slot reuse."""
+    from paper_2211_08506_b200.loader import GridPipeline, pinned_csr
+
+    cfg = synth.CONFIGS[4]
+    spec = spec_of(cfg)
+    batches = [synth.packed_batch(cfg, range(s, s + n)) for s, n in ((0, 7), (40, 13), (99, 5))]
+    refs = []
+    for pb in batches:
+        g, st = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+        refs.append((g.cpu().numpy(), st.cpu().numpy()))
+    pipe = GridPipeline(spec)
+    outs = []
+    for rnd in range(2):
+        for pb, (g_ref, st_ref) in zip(batches, refs):
+            if rnd == 0:
+                res = pipe.submit(*pinned_csr(pb.offsets, pb.channels, pb.xyz))
+            else:
+                res = pipe.submit(torch.from_numpy(pb.offsets).cuda(),
+                                  torch.from_numpy(pb.channels).cuda(),
+                                  torch.from_numpy(pb.xyz).cuda())
+            res.ready.synchronize()
+            outs.append((res.grids.cpu().numpy(), res.stats.cpu().numpy(), g_ref, st_ref))
+    for g, st, g_ref, st_ref in outs:
+        assert_bitwise(g, g_ref, "pipeline")
+        assert np.array_equal(st, st_ref)
