@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="timing plumbing backend (nccl; gloo to run several ranks on one GPU)")
     return ap.parse_args()
 
 
@@ -268,8 +270,9 @@ def run_b200(args):
     import torch
 
     world, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only for plumbing tests
     torch.cuda.set_device(local)
-    dist = Dist(world, rank, local)
+    dist = Dist(world, rank, local, backend=args.dist_backend)
     import paper_2211_08506_b200 as vg
     from paper_2211_08506_b200 import _native, shard, synth
 
