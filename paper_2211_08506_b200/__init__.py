@@ -26,6 +26,19 @@ from .gridgen import (
     generate_packed,
 )
 from .kernels import ERF_C1, ERF_C2, AxisTable, axis_tables_batch, erf_approx, fused_axis_tables
+from .io import (
+    ELEMENT_SYMBOLS,
+    MoleculeFile,
+    ParseError,
+    grid_from_array,
+    pack_molecules,
+    parse_points_csv,
+    parse_xyz,
+    read_npy,
+    write_npy,
+)
+from .loader import GridPipeline
+from .cli import cli_main
 
 __version__ = "0.1.0"
 
@@ -62,5 +75,16 @@ __all__ = [
     "erf_approx",
     "fused_axis_tables",
     "GaussianVoxelizer",
+    "ELEMENT_SYMBOLS",
+    "MoleculeFile",
+    "ParseError",
+    "grid_from_array",
+    "pack_molecules",
+    "parse_points_csv",
+    "parse_xyz",
+    "read_npy",
+    "write_npy",
+    "GridPipeline",
+    "cli_main",
     "__version__",
 ]

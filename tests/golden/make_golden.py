@@ -231,7 +231,94 @@ def make_configs():
     (HERE / "configs.json").write_text(json.dumps(out, indent=1))
 
 
+IO_XYZ = [
+    "1\n\nC 0 0 0\n",
+    "3\nwater\nO 0.0 0.0 0.117\nH 0.0 0.757 -0.467\nH 0.0 -0.757 -0.467\n",
+    "5\nmethane\nC 0.0 0.0 0.0\nH 0.629 0.629 0.629\nH -0.629 -0.629 0.629\n"
+    "H -0.629 0.629 -0.629\nH 0.629 -0.629 -0.629\n",
+    "4\nmixed\nFe 1 2 3\n\nZn 1.5 2 3\nS 0 0 -1e-3\nP 4 4 4\n",
+    "3\ncomment\nC 0 0 0\nC 1 0 0\n",
+    "1\n\nC 0 0 0\nC 1 0 0\n",
+    "1\n\nXx 0 0 0\n",
+    "1\n\nC 0 zero 0\n",
+    "banana\n\nC 0 0 0\n",
+    "-2\n\n",
+    "",
+    "2\n\nC 0 0 0 9\nH 1 1 1\n",
+    "1\n\nC nan 0 0\n",
+]
+IO_CSV = [
+    "0,0.5,0.5,0.5\n1,0.0,0.1,0.2\n",
+    "channel,x,y,z\n2,1,2,3\n\n0,4,5,6\n",
+    "",
+    "0,1,2\n",
+    "a,1,2,3\n",
+    "1,1,2,3\n-1,0,0,0\n",
+    "0,1,x,3\n",
+    "0,1,inf,3\n",
+    '0,"1,2",3\n',
+]
+
+
+def make_io():
+    from voxgrid.io import parse_points_csv, parse_xyz
+    from voxgrid.cli import cli_main
+    from voxgrid.bench import synth_corpus
+    import tempfile
+
+    out = {"xyz": [], "csv": [], "cli": [], "corpus": {}}
+    for text in IO_XYZ:
+        try:
+            m = parse_xyz(text)
+            out["xyz"].append({"text": text, "symbols": list(m.symbols),
+                               "positions": m.positions.tolist(),
+                               "auto": m.channel_map("auto"), "n_auto": m.n_channels("auto")})
+        except ValueError as exc:
+            out["xyz"].append({"text": text, "error": str(exc), "line": getattr(exc, "line", None)})
+    for text in IO_CSV:
+        try:
+            ps = parse_points_csv(text)
+            out["csv"].append({"text": text, "rows": ps.to_rows().tolist()})
+        except ValueError as exc:
+            out["csv"].append({"text": text, "error": str(exc), "line": getattr(exc, "line", None)})
+    with tempfile.TemporaryDirectory() as tmp:
+        tmp = Path(tmp)
+        (tmp / "water.xyz").write_text(IO_XYZ[1])
+        (tmp / "mixed.xyz").write_text(IO_XYZ[3])
+        (tmp / "pts.csv").write_text(IO_CSV[0])
+        runs = [
+            ["--input", "water.xyz", "--grid-size", "24", "--variance", "0.4"],
+            ["--input", "water.xyz", "--grid-size", "16,20,12", "--variance", "0.5",
+             "--channels", "single", "--mode", "dense"],
+            ["--input", "mixed.xyz", "--grid-size", "20", "--variance", "0.3", "--channels", "6",
+             "--padding-sigmas", "2.5"],
+            ["--input", "pts.csv", "--grid-size", "32", "--variance", "0.05", "--channels", "2",
+             "--box", "0,0,0,1,1,1"],
+            ["--input", "pts.csv", "--grid-size", "24", "--variance", "0.1", "--periodic",
+             "1,1,1"],
+        ]
+        for args in runs:
+            full = ["grid"] + [str(tmp / a) if a.endswith((".xyz", ".csv")) else a for a in args]
+            full += ["--output", str(tmp / "o.npy"), "--stats", str(tmp / "s.json")]
+            code = cli_main(full)
+            rec = {"args": args, "code": code}
+            if code == 0:
+                arr = np.load(tmp / "o.npy")
+                st = json.loads((tmp / "s.json").read_text())
+                st.pop("elapsed_ms", None)
+                rec.update(sha=sha(arr), shape=list(arr.shape), stats=st)
+            out["cli"].append(rec)
+    corpus = synth_corpus(7, (8, 40), 48.0, seed=3)
+    h = hashlib.sha256()
+    for ps in corpus:
+        h.update(ps.channels.astype(np.int64).tobytes())
+        h.update(ps.positions.astype(np.float64).tobytes())
+    out["corpus"] = {"n": 7, "seed": 3, "sha": h.hexdigest()}
+    (HERE / "io.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
+    make_io()
     make_erf()
     make_tables()
     n = make_grids()
