@@ -38,6 +38,18 @@ from .io import (
     write_npy,
 )
 from .loader import GridPipeline
+from .reversal import (
+    CountMismatchWarning,
+    Peak,
+    PeakSet,
+    ReversalConfig,
+    ReversalState,
+    detect_peaks,
+    loss,
+    loss_gradient,
+    refine_coords,
+    reverse_grid,
+)
 from .cli import cli_main
 
 __version__ = "0.1.0"
@@ -85,6 +97,16 @@ __all__ = [
     "read_npy",
     "write_npy",
     "GridPipeline",
+    "CountMismatchWarning",
+    "Peak",
+    "PeakSet",
+    "ReversalConfig",
+    "ReversalState",
+    "detect_peaks",
+    "loss",
+    "loss_gradient",
+    "refine_coords",
+    "reverse_grid",
     "cli_main",
     "__version__",
 ]

@@ -48,6 +48,15 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+// shared by the other translation units of the library (vg_reversal.cu)
+extern "C" int vg_internal_set_error(int code, const char* msg) {
+  return set_error(code, "%s", msg);
+}
+
+namespace {
+
 int check_launch(const char* what) {
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(VG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(err));

@@ -1,0 +1,258 @@
+// vg_reversal.cu — sm_100a kernels for grid reversal.
+//
+// The reversal (reference reversal.py) descends the grid-space MSE from seed
+// coordinates; every iteration regenerates candidate grids (the hot path,
+// vg_generate_f32) and needs
+//   * the loss  _mse (reversal.py:226-228): mean((regen - ref)^2) in fp64 —
+//     vg_mse_f64 does G candidate grids at once, two-pass fixed-order
+//     reduction (deterministic);
+//   * the analytic gradient _gradient_from_diff (reversal.py:240-276):
+//     per atom and axis, 2/N * sum over the support block of
+//     (regen - ref) * f_x[i] f_y[j] f_z[k] in fp64, where the axis' factor is
+//     the derivative table (axis_gradient, kernels.py:277-296, built on
+//     erf_approx_derivative, kernels.py:73-98) and the other two are the value
+//     tables — vg_loss_gradient_f64, one CTA per atom, tables in shared memory.
+// Bits follow the reference where it matters for the path (value tables are
+// the K1 numerics); the fp64 sums and float32 expm1 of the derivative are
+// tolerance-level.
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/voxgrid_b200.h"
+#include "vg_math.cuh"
+
+#define VG_API extern "C" __attribute__((visibility("default")))
+
+// error plumbing lives in vg_kernels.cu
+extern "C" int vg_internal_set_error(int code, const char* msg);
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMseBlocks = 296;     // partial sums per grid (2 x 148 SMs)
+constexpr int kMseThreads = 256;
+constexpr int kGradThreads = 256;
+constexpr int kGradMaxAxis = 1024;  // per-axis table length staged in shared memory
+
+int fail(int code, const char* what, cudaError_t e) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  return vg_internal_set_error(code, buf);
+}
+
+__device__ double block_reduce_f64(double v, double* red) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nw; ++w) t += red[w];
+  return t;  // thread 0
+}
+
+// pass 1: partial[g * kMseBlocks + blk] = sum over a fixed voxel range
+__global__ void __launch_bounds__(kMseThreads) vg_mse_partial_kernel(const float* __restrict__ ref,
+                                                                     const float* __restrict__ grids,
+                                                                     int64_t n, double* partial) {
+  __shared__ double red[kMseThreads / 32];
+  const int g = blockIdx.y;
+  const int64_t per = (n + kMseBlocks - 1) / kMseBlocks;
+  const int64_t lo = (int64_t)blockIdx.x * per, hi = min(n, lo + per);
+  const float* gr = grids + (int64_t)g * n;
+  double acc = 0.0;
+  for (int64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+    const double d = (double)__ldg(gr + v) - (double)__ldg(ref + v);
+    acc = __dadd_rn(acc, __dmul_rn(d, d));
+  }
+  const double t = block_reduce_f64(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)g * kMseBlocks + blockIdx.x] = t;
+}
+
+// pass 2: out[g] = (sum of partials in order) / n
+__global__ void vg_mse_final_kernel(const double* partial, int64_t n, double* out) {
+  __shared__ double red[32];
+  const int g = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < kMseBlocks; b += blockDim.x) acc += partial[(int64_t)g * kMseBlocks + b];
+  const double t = block_reduce_f64(acc, red);
+  if (threadIdx.x == 0) out[g] = t / (double)n;
+}
+
+// Exact derivative of the Bürmann erf, op order of kernels.py:84-97 (fp32).
+// expm1 is CUDA's (numpy's float32 expm1 may differ by an ulp: tolerance-level).
+__device__ __forceinline__ float erf_deriv_f32(float t) {
+  const float one = 1.0f;
+  const float t2 = __fmul_rn(t, t);
+  const float u = vg_exp_f32(-t2);
+  const float phi = (t2 == 0.0f) ? one : __fdiv_rn(-expm1f(-t2), t2);
+  const float sp = __fsqrt_rn(phi);
+  const float poly = __fadd_rn(one, __fmul_rn(__fmul_rn(VG_ERF_A, u), __fsub_rn(VG_ERF_C1, __fmul_rn(VG_ERF_C2, u))));
+  const float dpoly = __fmul_rn(VG_ERF_A, __fsub_rn(VG_ERF_C1, __fmul_rn(__fmul_rn(2.0f, VG_ERF_C2), u)));
+  const float inner = __fsub_rn(__fdiv_rn(poly, sp), __fmul_rn(__fmul_rn(__fmul_rn(2.0f, t2), sp), dpoly));
+  return __fmul_rn(u, inner);
+}
+
+struct GradParams {
+  const double* xyz;
+  const int32_t* channel;
+  const float* ref;
+  const float* regen;
+  double* grad;
+  double origin[3], delta[3];
+  double scale;     // 1/(sigma*sqrt(2))
+  float gscale;     // fl32(0.5/(sigma*sqrt(2)))
+  double inv_n2;    // 2/N
+  int n[3];         // voxels along x, y, z  (W, H, D)
+  int H, W, D, C;
+};
+
+// One CTA per atom: value + derivative tables of its 3 axes in shared memory,
+// then per axis the fp64 block sum over (derivative support on that axis) x
+// (value supports on the other two), reversal.py:255-275.
+__global__ void __launch_bounds__(kGradThreads) vg_grad_kernel(const __grid_constant__ GradParams p) {
+  __shared__ float val[3][kGradMaxAxis];
+  __shared__ float der[3][kGradMaxAxis];
+  __shared__ float edge_e[kGradMaxAxis + 1];
+  __shared__ float edge_d[kGradMaxAxis + 1];
+  __shared__ int vsup[3][2], gsup[3][2];
+  __shared__ double red[kGradThreads / 32];
+  const int a = blockIdx.x;
+  const int c = p.channel[a];
+  for (int ax = 0; ax < 3; ++ax) {
+    const int n = p.n[ax];
+    const double rel = __dsub_rn(p.origin[ax], p.xyz[a * 3 + ax]);
+    __syncthreads();
+    for (int e = threadIdx.x; e <= n; e += blockDim.x) {
+      const float t = vg_edge_arg(rel, p.delta[ax], e, p.scale);
+      edge_e[e] = vg_erf_f32(t);
+      edge_d[e] = erf_deriv_f32(t);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      val[ax][e] = __fmul_rn(0.5f, __fsub_rn(edge_e[e + 1], edge_e[e]));
+      der[ax][e] = __fmul_rn(p.gscale, __fsub_rn(edge_d[e], edge_d[e + 1]));
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // supports: first/last nonzero, (0,0) if none
+      int vlo = n, vhi = -1, glo = n, ghi = -1;
+      for (int e = threadIdx.x; e < n; e += 32) {
+        if (val[ax][e] != 0.0f) { vlo = min(vlo, e); vhi = max(vhi, e); }
+        if (der[ax][e] != 0.0f) { glo = min(glo, e); ghi = max(ghi, e); }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        vlo = min(vlo, __shfl_xor_sync(kFull, vlo, off));
+        vhi = max(vhi, __shfl_xor_sync(kFull, vhi, off));
+        glo = min(glo, __shfl_xor_sync(kFull, glo, off));
+        ghi = max(ghi, __shfl_xor_sync(kFull, ghi, off));
+      }
+      if (threadIdx.x == 0) {
+        vsup[ax][0] = vhi < 0 ? 0 : vlo;
+        vsup[ax][1] = vhi < 0 ? 0 : vhi + 1;
+        gsup[ax][0] = ghi < 0 ? 0 : glo;
+        gsup[ax][1] = ghi < 0 ? 0 : ghi + 1;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t slab = (int64_t)p.W * p.D;
+  const float* ref_c = p.ref + (int64_t)c * p.H * slab;
+  const float* reg_c = p.regen + (int64_t)c * p.H * slab;
+  for (int axis = 0; axis < 3; ++axis) {
+    int lo[3], hi[3];
+    for (int q = 0; q < 3; ++q) {
+      lo[q] = q == axis ? gsup[q][0] : vsup[q][0];
+      hi[q] = q == axis ? gsup[q][1] : vsup[q][1];
+    }
+    double acc = 0.0;
+    const int nx = hi[0] - lo[0], ny = hi[1] - lo[1], nz = hi[2] - lo[2];
+    if (nx > 0 && ny > 0 && nz > 0 && gsup[axis][1] > gsup[axis][0]) {
+      const float* fx = axis == 0 ? der[0] : val[0];
+      const float* fy = axis == 1 ? der[1] : val[1];
+      const float* fz = axis == 2 ? der[2] : val[2];
+      const int64_t total = (int64_t)nx * ny * nz;
+      for (int64_t v = threadIdx.x; v < total; v += blockDim.x) {
+        const int k = lo[2] + (int)(v % nz);
+        const int64_t r = v / nz;
+        const int i = lo[0] + (int)(r % nx);
+        const int j = lo[1] + (int)(r / nx);
+        const int64_t off = (int64_t)j * slab + (int64_t)i * p.D + k;
+        const double d = (double)reg_c[off] - (double)ref_c[off];
+        acc += d * (double)fx[i] * (double)fy[j] * (double)fz[k];
+      }
+    }
+    const double t = block_reduce_f64(acc, red);
+    if (threadIdx.x == 0) p.grad[a * 3 + axis] = p.inv_n2 * t;
+  }
+}
+
+}  // namespace
+
+VG_API size_t vg_mse_workspace_bytes(int64_t n_voxels, int32_t n_grids) {
+  (void)n_voxels;
+  return (size_t)(n_grids > 0 ? n_grids : 0) * kMseBlocks * sizeof(double);
+}
+
+VG_API int vg_mse_f64(const float* ref, const float* grids, int64_t n_voxels, int32_t n_grids,
+                      double* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_voxels <= 0 || n_grids < 0)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: need n_voxels > 0, n_grids >= 0");
+  if (n_grids == 0) return VG_OK;
+  if (ref == nullptr || grids == nullptr || out == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: NULL pointer");
+  if (workspace == nullptr || workspace_bytes < vg_mse_workspace_bytes(n_voxels, n_grids))
+    return vg_internal_set_error(VG_ERR_WORKSPACE, "vg_mse_f64: workspace too small");
+  if (n_grids > 65535) return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: too many grids");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* partial = static_cast<double*>(workspace);
+  vg_mse_partial_kernel<<<dim3(kMseBlocks, n_grids), kMseThreads, 0, st>>>(ref, grids, n_voxels,
+                                                                            partial);
+  vg_mse_final_kernel<<<n_grids, 256, 0, st>>>(partial, n_voxels, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_mse_f64", e);
+}
+
+VG_API int vg_loss_gradient_f64(const vg_batch_desc* desc, const float* ref, const float* regen,
+                                double* grad, void* stream) {
+  if (desc == nullptr || ref == nullptr || regen == nullptr || grad == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: NULL pointer");
+  const vg_batch_desc& d = *desc;
+  if (d.n_atoms == 0) return VG_OK;
+  if (d.periodic)
+    return vg_internal_set_error(VG_ERR_INVALID,
+                                 "reversal of periodic grids is not supported (open boundaries)");
+  if (d.W > kGradMaxAxis || d.H > kGradMaxAxis || d.D > kGradMaxAxis)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: axis longer than 1024");
+  if (d.xyz == nullptr || d.channel == nullptr || !(d.scale > 0.0))
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: bad descriptor");
+  GradParams p;
+  memset(&p, 0, sizeof p);
+  p.xyz = d.xyz;
+  p.channel = d.channel;
+  p.ref = ref;
+  p.regen = regen;
+  p.grad = grad;
+  for (int a = 0; a < 3; ++a) {
+    p.origin[a] = d.origin[a];
+    p.delta[a] = d.delta[a];
+  }
+  p.scale = d.scale;
+  // fl32(0.5 / (sigma * sqrt(2))) = fl32(0.5 * scale) exactly (power-of-two factor)
+  p.gscale = (float)(0.5 * d.scale);
+  p.n[0] = d.W;
+  p.n[1] = d.H;
+  p.n[2] = d.D;
+  p.H = d.H;
+  p.W = d.W;
+  p.D = d.D;
+  p.C = d.C;
+  p.inv_n2 = 2.0 / ((double)d.C * d.H * d.W * d.D);
+  vg_grad_kernel<<<(unsigned)d.n_atoms, kGradThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_loss_gradient_f64", e);
+}

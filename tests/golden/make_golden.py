@@ -317,7 +317,63 @@ def make_io():
     (HERE / "io.json").write_text(json.dumps(out, indent=1))
 
 
+def make_reversal():
+    """Peaks (exact), loss/gradient values and full reversals by the reference."""
+    import warnings
+    from voxgrid import (ReversalState, detect_peaks, loss, loss_gradient, refine_coords,
+                         reverse_grid)
+
+    rng = np.random.default_rng(4242)
+    box = BoundingBox((0.0, 0.0, 0.0), (12.0, 12.0, 12.0))
+    spec = GridSpec((24, 24, 24), 2, box, 0.5)
+    cases = []
+    for trial in range(6):
+        n = int(rng.integers(1, 7))
+        pts = []
+        while len(pts) < n:
+            p = rng.uniform(2.05, 9.95, size=3)
+            if all(np.linalg.norm(p - q) >= 3.0 for q in pts):
+                pts.append(p)
+        truth = ParticleSet(rng.integers(0, 2, size=n), np.array(pts))
+        grid, _ = generate_grid(truth, spec)
+        peaks = detect_peaks(grid)
+        cand = truth.positions + rng.uniform(-0.3, 0.3, size=(n, 3))
+        st = ReversalState(truth.channels.copy(), cand)
+        lval = loss(grid, st)
+        gval = loss_gradient(grid, st)
+        refined = refine_coords(grid, st)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            rec = reverse_grid(grid)
+        cases.append(dict(
+            chans=truth.channels.tolist(), pos=truth.positions.tolist(), cand=cand.tolist(),
+            peaks=[[p.channel, list(p.index), p.value, p.persistence, list(p.seed)]
+                   for p in peaks],
+            loss=lval, grad=gval.tolist(),
+            refined=dict(pos=refined.positions.tolist(), loss=refined.loss,
+                         iterations=refined.iterations, converged=refined.converged),
+            reversed=rec.to_rows().tolist()))
+    # peak detection on random (noisy, plateau-rich) grids
+    rnd = []
+    r2 = np.random.default_rng(123)
+    small = GridSpec((8, 8, 8), 1, BoundingBox((0, 0, 0), (1, 1, 1)), 0.1)
+    for trial in range(8):
+        data = r2.uniform(0.0, 1.0, size=(1, 8, 8, 8)).astype(np.float32)
+        if trial % 3 == 0:
+            data[data < 0.3] = 0.0
+        if trial % 4 == 0:
+            data = np.round(data, 1).astype(np.float32)
+        thr = float(r2.uniform(0.05, 0.6))
+        from voxgrid import Grid as RGrid
+        peaks = detect_peaks(RGrid(small, np.ascontiguousarray(data)), thr)
+        rnd.append(dict(data=data.ravel().tolist(), threshold=thr,
+                        peaks=[[p.channel, list(p.index), p.value, p.persistence] for p in peaks]))
+    (HERE / "reversal.json").write_text(json.dumps({"spec": [24, 2, 12.0, 0.5], "cases": cases,
+                                                   "random_peaks": rnd}))
+
+
 if __name__ == "__main__":
+    make_reversal()
     make_io()
     make_erf()
     make_tables()

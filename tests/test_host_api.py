@@ -204,8 +204,11 @@ def test_estimator_box_modes_and_validation():
             est.fit(bad)
     with pytest.raises(ValueError):
         vg.GaussianVoxelizer(grid_size=(4, 4)).fit(sample_clouds())._shape()
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(ValueError):
         est.fit(sample_clouds()).inverse_transform(None)
+    with pytest.raises(ValueError):
+        vg.GaussianVoxelizer(box="per-sample").fit(sample_clouds()).inverse_transform(
+            np.zeros((1, 1, 4, 4, 4), np.float32))
 
 
 def test_synth_configs_follow_baseline():

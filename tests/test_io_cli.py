@@ -116,8 +116,8 @@ def test_cli_argument_errors(tmp_path, capsys):
     assert cli.cli_main(["grid", "--input", str(tmp_path / "m.xyz"), "--variance", "0.5",
                          "--periodic", "1,1,1", "--box", "0,0,0,1,1,1",
                          "--output", str(tmp_path / "o.npy")]) == 1
-    assert cli.cli_main(["reverse", "--input", "g.npy", "--variance", "0.5",
-                         "--output", "o.csv"]) == 1
+    assert cli.cli_main(["reverse", "--input", str(tmp_path / "none.npy"), "--variance", "0.5",
+                         "--output", "o.csv"]) == 1  # missing file -> OSError -> 1
     assert cli.cli_main(["grid", "--grid-size", "1,2", "--input", "a", "--variance", "1",
                          "--output", "o"]) == 2
 
