@@ -385,7 +385,7 @@ def run_b200(args):
     st_h = torch.empty((Bl, 2), dtype=torch.int64).pin_memory()
     h2d = off_h.numel() * 8 + ch_h.numel() * 4 + xyz_h.numel() * 8
     d2h = st_h.numel() * 8
-    epipe = GridPipeline(spec, dev)
+    epipe = pipe  # reuse its double buffers (large configs: 2 x 43 GB at cfg2)
 
     def e2e_step():
         res = epipe.submit(off_h, ch_h, xyz_h)

@@ -127,6 +127,17 @@ __device__ __forceinline__ int64_t owner_of(const int64_t* offsets, int64_t n_mo
   return lo;
 }
 
+// E(t_e) for one edge per lane, warp-uniform: the series runs only when some
+// valid lane of the warp is unsaturated; otherwise each lane takes the exact
+// saturated value vg_erf_sat_f32 would return (+-1). Invalid lanes give 0.
+__device__ __forceinline__ float edge_erf_warp(bool valid, double rel, double d, int e, double s) {
+  const float t = vg_edge_arg(rel, d, e, s);
+  const bool live = valid && !(fabsf(t) >= VG_TSAT);
+  float v = valid ? (t >= VG_TSAT ? 1.0f : -1.0f) : 0.0f;
+  if (__any_sync(kFull, live) && valid) v = vg_erf_sat_f32(t);
+  return v;
+}
+
 __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * (kTableThreads / 32) + (threadIdx.x >> 5);
@@ -163,20 +174,22 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p)
   }
 
   float* tbl = p.tbl[axis] + atom * p.row[axis];
+  const int c_start = 0;
   float e_cur[3], e_nxt[3];
 #pragma unroll
   for (int im = 0; im < 3; ++im) {
     e_cur[im] = 0.0f;
-    if (im < images && lane <= n) e_cur[im] = vg_erf_sat_f32(vg_edge_arg(rel[im], d, lane, s));
+    const int e0 = c_start + lane;
+    if (im < images) e_cur[im] = edge_erf_warp(e0 >= 0 && e0 <= n, rel[im], d, e0, s);
   }
   int lo = -1, hi = 0;
-  for (int c0 = 0; c0 < n; c0 += 32) {
+  for (int c0 = c_start; c0 < n; c0 += 32) {
     const int e = c0 + lane;
     // erf at the next chunk's edges (each edge evaluated exactly once)
 #pragma unroll
     for (int im = 0; im < 3; ++im) {
       e_nxt[im] = 0.0f;
-      if (im < images && e + 32 <= n) e_nxt[im] = vg_erf_sat_f32(vg_edge_arg(rel[im], d, e + 32, s));
+      if (im < images) e_nxt[im] = edge_erf_warp(e + 32 <= n, rel[im], d, e + 32, s);
     }
     float g = 0.0f;
 #pragma unroll
@@ -191,8 +204,8 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p)
       }
     }
     if (p.has_threshold && !(g >= p.threshold)) g = 0.0f;  // kernels.py:271-272
-    if (e < n) tbl[e] = g;
-    const unsigned nz = __ballot_sync(kFull, e < n && g != 0.0f);
+    if (e >= 0 && e < n) tbl[e] = g;
+    const unsigned nz = __ballot_sync(kFull, e >= 0 && e < n && g != 0.0f);
     if (nz != 0u) {
       if (lo < 0) lo = c0 + __ffs(nz) - 1;
       hi = c0 + 32 - __clz(nz);
@@ -203,6 +216,110 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p)
   if (lane == 0) {
     const int slo = lo < 0 ? 0 : lo;   // _support_of: (0, 0) when all zero
     const int shi = lo < 0 ? 0 : hi;
+    p.supp[atom * 4 + axis] = slo | (shi << 16);
+    if (axis == 0) p.supp[atom * 4 + 3] = p.channel[atom];
+  }
+}
+
+// Open axes: one thread per (atom, axis) row. Only edges inside the row's
+// unsaturated window need the erf series; the window [a, b] is found exactly
+// (t_e is monotone in e, so a = first edge with t_e > -t_sat and b = last edge
+// with t_e < t_sat, checked with the same fp32 edge arguments), every g_e
+// outside [a-1, b] is 0.5*(E-E) with both E equal to -1 or +1, i.e. +0.
+// Window values go through a per-warp shared buffer so each row is then
+// written by the whole warp with coalesced stores; rows are grouped by axis
+// (blockIdx.y) so the warp shares n and the table.
+constexpr int kWin = 32;   // window edges buffered per lane per pass
+
+__device__ __forceinline__ bool below_sat(float t) { return t <= -VG_TSAT; }
+__device__ __forceinline__ bool above_sat(float t) { return t >= VG_TSAT; }
+
+__global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TableParams p) {
+  __shared__ float wbuf[kTableThreads / 32][32][kWin + 1];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int axis = blockIdx.y;
+  const int n = p.n[axis];
+  const int64_t atom = (int64_t)blockIdx.x * kTableThreads + threadIdx.x;
+  const bool valid = atom < p.n_atoms;
+
+  double rel = 0.0, d = 1.0;
+  int glo = 0, ghi = -1;   // candidate g range (empty for invalid lanes)
+  if (valid) {
+    double o = p.origin[axis];
+    d = p.delta[axis];
+    if (p.mol_origin != nullptr || p.mol_delta != nullptr) {
+      const int64_t b = owner_of(p.offsets, p.n_molecules, atom);
+      if (p.mol_origin != nullptr) o = p.mol_origin[b * 3 + axis];
+      if (p.mol_delta != nullptr) d = p.mol_delta[b * 3 + axis];
+    }
+    rel = __dsub_rn(o, p.xyz[atom * 3 + axis]);   // kernels.py:253
+    const double s = p.scale;
+    glo = 0;
+    ghi = n - 1;
+    if (d > 0.0 && isfinite(rel) && isfinite(d)) {
+      // estimates, then exact correction against the fp32 edge arguments
+      const double ea = (-(double)VG_TSAT / s - rel) / d;
+      const double eb = ((double)VG_TSAT / s - rel) / d;
+      int a = ea <= 0.0 ? 0 : (ea >= (double)(n + 1) ? n + 1 : (int)ceil(ea));
+      int b = eb < 0.0 ? -1 : (eb >= (double)n ? n : (int)floor(eb));
+      while (a > 0 && !below_sat(vg_edge_arg(rel, d, a - 1, s))) --a;
+      while (a <= n && below_sat(vg_edge_arg(rel, d, a, s))) ++a;
+      while (b < n && !above_sat(vg_edge_arg(rel, d, b + 1, s))) ++b;
+      while (b >= 0 && above_sat(vg_edge_arg(rel, d, b, s))) --b;
+      glo = max(0, a - 1);
+      ghi = min(n - 1, b);
+    }
+  }
+
+  float* tbl_axis = p.tbl[axis];
+  const int64_t row = p.row[axis];
+  const int64_t atom0 = atom - lane;
+  int cur = glo;                 // next window edge this lane computes
+  int nz_lo = -1, nz_hi = 0;
+  float e_prev = 0.0f;
+  if (cur <= ghi) e_prev = vg_erf_sat_f32(vg_edge_arg(rel, d, cur, p.scale));
+  bool first = true;
+  for (;;) {
+    // pass: up to kWin window values per lane into the warp buffer
+    const int pstart = cur;
+    const int pend = min(ghi + 1, cur + kWin);
+    for (int e = pstart; e < pend; ++e) {
+      const float e_next = vg_erf_sat_f32(vg_edge_arg(rel, d, e + 1, p.scale));
+      float g = VG_FMUL(0.5f, VG_FSUB(e_next, e_prev));       // kernels.py:260
+      if (p.has_threshold && !(g >= p.threshold)) g = 0.0f;   // kernels.py:271-272
+      if (g != 0.0f) {
+        if (nz_lo < 0) nz_lo = e;
+        nz_hi = e + 1;
+      }
+      wbuf[warp][lane][e - pstart] = g;
+      e_prev = e_next;
+    }
+    cur = max(pend, cur);
+    __syncwarp();
+    // coalesced write-out, one row at a time
+    for (int r = 0; r < 32; ++r) {
+      const int r_lo = __shfl_sync(kFull, glo, r);
+      const int r_hi = __shfl_sync(kFull, ghi, r);
+      const int r_ps = __shfl_sync(kFull, pstart, r);
+      const int r_pe = __shfl_sync(kFull, pend, r);
+      if (atom0 + r >= p.n_atoms) break;
+      if (!first && r_pe <= r_ps) continue;
+      float* dst = tbl_axis + (atom0 + r) * row;
+      for (int c0 = 0; c0 < n; c0 += 32) {
+        const int e = c0 + lane;
+        if (e >= n) break;
+        if (e >= r_ps && e < r_pe) dst[e] = wbuf[warp][r][e - r_ps];
+        else if (first && (e < r_lo || e > r_hi)) dst[e] = 0.0f;
+      }
+    }
+    first = false;
+    if (!__any_sync(kFull, cur <= ghi)) break;
+    __syncwarp();
+  }
+  if (valid) {
+    const int slo = nz_lo < 0 ? 0 : nz_lo;   // _support_of: (0, 0) when all zero
+    const int shi = nz_lo < 0 ? 0 : nz_hi;
     p.supp[atom * 4 + axis] = slo | (shi << 16);
     if (axis == 0) p.supp[atom * 4 + 3] = p.channel[atom];
   }
@@ -883,6 +1000,11 @@ int launch_tables(const vg_batch_desc* d, const vg_ws_layout& L, char* ws, cudaS
   p.has_threshold = !std::isnan(d->threshold);
   p.threshold = d->threshold;
   p.periodic = d->periodic != 0;
+  if (!p.periodic) {
+    const int64_t blocks = (d->n_atoms + kTableThreads - 1) / kTableThreads;
+    vg_tables_open_kernel<<<dim3((unsigned)blocks, 3), kTableThreads, 0, st>>>(p);
+    return check_launch("vg_tables_open_kernel");
+  }
   const int64_t warps = d->n_atoms * 3;
   const int64_t blocks = (warps + kTableThreads / 32 - 1) / (kTableThreads / 32);
   vg_tables_kernel<<<(unsigned)blocks, kTableThreads, 0, st>>>(p);

@@ -66,8 +66,11 @@ class GridPipeline:
         self.engine = GridEngine(self.device)
         self.lib = _native.lib()
         with torch.cuda.device(self.device):
+            # K1 (short, compute-bound) runs at high priority so its blocks are
+            # dispatched as soon as K3 blocks of the previous batch retire,
+            # instead of queueing behind K3's whole grid
             self.copy_stream = torch.cuda.Stream(self.device)
-            self.tables_stream = torch.cuda.Stream(self.device)
+            self.tables_stream = torch.cuda.Stream(self.device, priority=-1)
             self.compute_stream = torch.cuda.Stream(self.device)
         self.slots = [_Slot() for _ in range(depth)]
         self.k = 0

@@ -73,6 +73,44 @@ def test_axis_tables_match_golden(case):
         assert list(tabs[a].support) == meta["supports"][a], (case, a)
 
 
+# K1 open-axis window search (exact saturation boundaries, multi-pass windows
+# wider than the 32-edge buffer, empty windows, one-edge jumps, thresholds,
+# per-molecule origins/deltas) against the oracle's full-row restatement.
+@pytest.mark.parametrize("sigma,shape,extent,thr", [
+    (0.5, (33, 64, 40), 12.0, None),     # typical window, odd counts
+    (3.0, (300, 257, 520), 15.0, None),  # windows of hundreds of edges
+    (0.004, (20, 17, 9), 10.0, None),    # window shorter than one edge
+    (0.7, (31, 65, 129), 20.0, 1e-4),    # threshold
+    (0.7, (31, 65, 129), 20.0, -1.0),    # negative threshold keeps zeros
+])
+def test_axis_tables_window_search_vs_oracle(sigma, shape, extent, thr):
+    rng = np.random.default_rng(int(sigma * 1000) + shape[0])
+    n_mol, per = 7, 111
+    n = n_mol * per
+    offsets = np.arange(0, n + 1, per, dtype=np.int64)
+    xyz = rng.uniform(-0.5 * extent, 1.5 * extent, size=(n, 3))   # many far outside
+    xyz[::17] = np.round(xyz[::17] * 4) / 4                        # edge-aligned centres
+    H, W, D = shape
+    spec = vg.GridSpec(shape, 1, vg.BoundingBox((0.0, 0.0, 0.0), (extent,) * 3), sigma)
+    mo = rng.uniform(-2.0, 2.0, size=(n_mol, 3))
+    md = np.array([[extent / W, extent / H, extent / D]]) * rng.uniform(0.8, 1.25, size=(n_mol, 1))
+    for per_mol in (False, True):
+        kw = {"mol_origin": mo, "mol_delta": md} if per_mol else {}
+        tx, ty, tz, sup = vg.axis_tables_batch(offsets, np.zeros(n, np.int32), xyz, spec,
+                                               threshold=thr, **kw)
+        got = [t.cpu().numpy() for t in (tx, ty, tz)]
+        sup = sup.cpu().numpy()
+        for a, cnt in enumerate((W, H, D)):
+            for b in range(n_mol):
+                o = mo[b, a] if per_mol else 0.0
+                d = md[b, a] if per_mol else extent / cnt
+                rows = slice(offsets[b], offsets[b + 1])
+                ref, rsup = orc.axis_tables(xyz[rows, a], cnt, o, d, sigma, threshold=thr)
+                assert np.array_equal(got[a][rows].view(np.uint32), ref.view(np.uint32)), \
+                    (per_mol, a, b)
+                assert np.array_equal(sup[rows, a], rsup), (per_mol, a, b)
+
+
 # ---------------------------------------------------------------------------
 # single grids: the reference's KAT-style cases
 # ---------------------------------------------------------------------------
