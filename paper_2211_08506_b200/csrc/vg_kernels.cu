@@ -73,9 +73,15 @@ constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bou
 #ifndef VG_ROW_MINB
 #define VG_ROW_MINB 4   // K3 row kernel: resident CTAs per SM the register budget targets
 #endif
-constexpr int kStageBytes = 24576;
+#ifndef VG_ROW_MINB1
+#define VG_ROW_MINB1 VG_ROW_MINB   // ... for one row step per CTA (M = 1)
+#endif
+constexpr int row_minb(int m) { return m == 1 ? VG_ROW_MINB1 : VG_ROW_MINB; }
+constexpr int kStageBytes = 24576;   // K3: shared-memory staging budget per CTA
 constexpr int kStageCapMax = 96;     // K3: staged candidates per sub-chunk (upper bound)
-constexpr int64_t kTaskBytes = 262144; // K3: output bytes per CTA (y-chunk sizing)   // K3: shared-memory staging budget per CTA
+constexpr int64_t kTaskBytes = 262144;       // K3: output bytes per CTA (y-chunk sizing)
+constexpr int64_t kFusedTaskBytes = 1048576; // ... per channel-fused CTA, all channels
+constexpr int64_t kMinCtas = 148 * 8;         // K3: CTAs a launch should at least offer
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -359,6 +365,7 @@ struct SlabParams {
   int stage_gz;         // offset of gz inside a staged block
   int stage_floats;     // floats of the staging area (sublists follow it)
   int c0_cap;           // level-0 candidate capacity (ints before the staging area)
+  int fuse_channels;    // 1: one CTA serves every channel (grid.y == 1)
 };
 
 struct SlabShared {
@@ -402,7 +409,7 @@ __device__ __forceinline__ int block_rank(bool keep, int* warp_cnt, int& total) 
 struct AtomFilter {
   int c, jlo, jhi, xa, xb, za, zb;
   __device__ __forceinline__ bool operator()(const int4& s) const {
-    return s.w == c && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
+    return (c < 0 || s.w == c) && lo16(s.x) < hi16(s.x) && lo16(s.z) < hi16(s.z) && lo16(s.y) < jhi &&
            hi16(s.y) > jlo && lo16(s.x) < xb && hi16(s.x) > xa && lo16(s.z) < zb &&
            hi16(s.z) > za;
   }
@@ -714,6 +721,38 @@ __device__ __forceinline__ void lds_slot2(Slot8& v, unsigned a, unsigned halfb) 
   lds_slot(v.b, a + halfb);
 }
 
+// One candidate term: ((gy*gx)*gz) added to the slot (kernels' op order).
+template <typename Slot>
+__device__ __forceinline__ void term_of(unsigned blk, unsigned gy_off, unsigned gxm, unsigned gz_off,
+                                        unsigned halfb, Slot& gz, float& pyx) {
+  lds_slot2(gz, blk + gz_off, halfb);
+  pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
+}
+
+// Walk the active entries `act` (ballot over a 32-entry group, ascending =
+// ascending atom order) two at a time: both entries' loads are issued before
+// the first one's adds, so one shared-memory latency covers two terms. The
+// adds stay in order, so the sums are unchanged.
+template <typename Slot>
+__device__ __forceinline__ void walk_group(unsigned act, int ent_x, unsigned gy_off, unsigned gxm,
+                                           unsigned gz_off, unsigned halfb, Slot& acc) {
+  while (act != 0u) {
+    const int b0 = __ffs(act) - 1;
+    act &= act - 1u;
+    const bool two = act != 0u;   // warp-uniform
+    const int b1 = two ? __ffs(act) - 1 : b0;
+    if (two) act &= act - 1u;
+    const unsigned blk0 = (unsigned)__shfl_sync(kFull, ent_x, b0);
+    const unsigned blk1 = (unsigned)__shfl_sync(kFull, ent_x, b1);
+    Slot gz0, gz1;
+    float p0, p1;
+    term_of(blk0, gy_off, gxm, gz_off, halfb, gz0, p0);
+    term_of(blk1, gy_off, gxm, gz_off, halfb, gz1, p1);
+    add_scaled(acc, p0, gz0);                                              // (..)(x)tz, +=
+    if (two) add_scaled(acc, p1, gz1);
+  }
+}
+
 template <int M, int SW, bool FIRST>
 __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int m_stride, int nj,
                                             int ibase, int row_end, int R, Counts<M> cnt,
@@ -721,6 +760,17 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
                                             unsigned gz_off, int half) {
   using Slot = typename SlotW<SW>::T;
   const unsigned halfb = 4u * (unsigned)half;
+  const int lane = (int)(threadIdx.x & 31);
+  // Sublists of <= 32 entries (the common case) are loaded once for all slabs.
+  // (M <= 4: the preloaded entries must not push the row loop into spills)
+  bool small = M <= 4;
+  int2 pre[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    small = small && cnt.v[m] <= 32;
+    pre[m] = make_int2(0, 0);
+    if (M <= 4 && lane < cnt.v[m]) pre[m] = lds_int2(lists_s + 8u * (unsigned)(m * cap + lane));
+  }
   int nz = 0;
   float* dst_j = base;
   for (int jj = 0; jj < nj; ++jj, dst_j += slab_elems) {
@@ -736,24 +786,21 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
         ld_slot(acc, dst, half);
         nz -= nonzeros_pos(acc);
       }
-      const unsigned L = lists_s + 8u * (unsigned)(m * cap);
       const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
-      // 32 entries at a time: each lane tests one entry's slab mask, the
-      // ballot gives the entries active on this slab, visited in ascending
-      // order (ascending atom order) with no cost for the inactive ones.
-      for (int c0 = 0; c0 < cnt.v[m]; c0 += 32) {
-        const int e = c0 + (int)(threadIdx.x & 31);
-        int2 mine_ent = make_int2(0, 0);
-        if (e < cnt.v[m]) mine_ent = lds_int2(L + 8u * (unsigned)e);
-        unsigned act = __ballot_sync(kFull, (mine_ent.y & jbit) != 0);
-        while (act != 0u) {
-          const int bit = __ffs(act) - 1;
-          act &= act - 1u;
-          const unsigned blk = (unsigned)__shfl_sync(kFull, mine_ent.x, bit);
-          Slot gz;
-          lds_slot2(gz, blk + gz_off, halfb);
-          const float pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
-          add_scaled(acc, pyx, gz);                                              // (..)(x)tz, +=
+      if (small) {
+        walk_group(__ballot_sync(kFull, (pre[m].y & jbit) != 0), pre[m].x, gy_off, gxm, gz_off,
+                   halfb, acc);
+      } else {
+        // 32 entries at a time: each lane tests one entry's slab mask, the
+        // ballot gives the entries active on this slab, visited in ascending
+        // order (ascending atom order) with no cost for the inactive ones.
+        const unsigned L = lists_s + 8u * (unsigned)(m * cap);
+        for (int c0 = 0; c0 < cnt.v[m]; c0 += 32) {
+          const int e = c0 + lane;
+          int2 ent = make_int2(0, 0);
+          if (e < cnt.v[m]) ent = lds_int2(L + 8u * (unsigned)e);
+          walk_group(__ballot_sync(kFull, (ent.y & jbit) != 0), ent.x, gy_off, gxm, gz_off, halfb,
+                     acc);
         }
       }
       if (mine) {
@@ -765,15 +812,70 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
   return nz;
 }
 
+// Stage gy (slabs js..je), gx (CTA rows) and gz (z window) of candidates
+// meta[0..ns) into consecutive blocks of the staging area, one warp per block.
+template <int SW>
+__device__ __forceinline__ void stage_tables(const SlabParams& p, const int4* meta, int ns,
+                                             float* stage, int js, int je, int row_base, int rows,
+                                             int zv0, int zv1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < ns; q += nw) {
+    const int64_t a = meta[q].w;
+    float* dst = stage + q * p.stage_stride;
+    for (int e = lane; e < je - js; e += 32) dst[e] = __ldg(p.ty + a * p.ry + js + e);
+    for (int e = lane; e < rows; e += 32)
+      dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + row_base + e);
+    if (SW >= 4) {
+      const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz + zv0);
+      float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
+      for (int e = lane; e < p.zw * (SW / 4); e += 32) dst4[e] = __ldg(src4 + e);
+    } else {
+      for (int e = lane; e < zv1 - zv0; e += 32) dst[p.stage_gz + e] = __ldg(p.tz + a * p.rz + zv0 + e);
+    }
+  }
+}
+
+// Warp-private ordered sublists: per row step m, the staged candidates (of
+// channel ch, or any channel if ch < 0) whose x-support meets this warp's
+// rows: {shared address of the block, slab mask}.
+template <int M>
+__device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* meta, int ns, int ch,
+                                               int2* lists, unsigned stage_s, int js, int je,
+                                               int rlo0, int rhi0, int R, Counts<M>& cnt) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int rlo = rlo0 + m * R, rhi = rhi0 + m * R;
+    int filled = 0;
+    for (int q0 = 0; q0 < ns; q0 += 32) {
+      const int q = q0 + lane;
+      bool hit = false;
+      int2 ent = make_int2(0, 0);
+      if (q < ns) {
+        const int4 s = meta[q];
+        hit = lo16(s.x) <= rhi && hi16(s.x) > rlo;
+        if (ch >= 0) hit = hit && __ldg(&p.supp[s.w].w) == ch;
+        const int lo = max(lo16(s.y), js) - js, hi = min(hi16(s.y), je) - js;
+        const unsigned long long mask = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
+        ent = make_int2((int)(stage_s + 4u * (unsigned)(q * p.stage_stride)), (int)(unsigned)mask);
+      }
+      const unsigned bal = __ballot_sync(kFull, hit);
+      if (hit) lists[m * p.stage_cap + filled + __popc(bal & ((1u << lane) - 1u))] = ent;
+      filled += __popc(bal);
+    }
+    cnt.v[m] = filled;
+  }
+}
+
 template <int M, int SW>
-__global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const __grid_constant__ SlabParams p) {
+__global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotW<SW>::T;
   constexpr int kWidth = SW;
   __shared__ SlabShared sh;
   extern __shared__ float4 dyn4[];
   int* c0 = reinterpret_cast<int*>(dyn4);             // level-0 candidates [c0_cap]
   float* stage = reinterpret_cast<float*>(dyn4) + p.c0_cap;  // staged tables, then sublists
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
 
   RowTile T;
   T.b = blockIdx.x;
@@ -792,7 +894,7 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
   T.a1 = __ldg(p.offsets + T.b + 1);
   const int j0 = chunk * p.jc;
   const int j1 = min(p.H, j0 + p.jc);
-  const int zw = p.zw, R = p.rows_per_step, spr = p.slots_per_row;
+  const int zw = p.zw, R = p.rows_per_step;
   T.r0 = div_magic(tid, p.zw_magic);
   T.k = zblk * zw + (tid - T.r0 * zw);
   T.wr0 = div_magic(warp * 32, p.zw_magic);
@@ -812,97 +914,90 @@ __global__ void __launch_bounds__(kRowThreads, VG_ROW_MINB) vg_slab_kernel(const
   const int half = SW == 8 ? 4 * zw : 0;
   const unsigned gz_off = 4u * (unsigned)(p.stage_gz + (zf - T.zv0));
   const unsigned gx_off = 4u * (unsigned)(p.stage_gx + T.r0);
-  float* out_c = p.out + (T.b * p.C + T.c) * (int64_t)p.H * p.slab_elems;
   const int slot0 = ibase * p.D + zf;  // float offset in the slab
+  const int rows = T.row_end - T.row_base;
+  const int rlo0 = T.row_base + T.wr0, rhi0 = T.row_base + T.wr1;
+  const int64_t chan_elems = (int64_t)p.H * p.slab_elems;
 
   int nz = 0;
-  // Level 0: the CTA's candidates over its whole chunk, scanned once from the
-  // molecule's atoms; sub-chunk lists below filter this short list instead.
-  // (skipped for small molecules: scanning them directly is as cheap)
-  const AtomFilter f0{T.c, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
-  const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x && p.c0_cap > 0
-                     ? build_index_list(p.supp, sh, c0, p.c0_cap, T.a0, T.a1, f0)
-                     : -1;
-  const int* src = n0 >= 0 ? c0 : nullptr;
-  const int64_t src_begin = n0 >= 0 ? 0 : T.a0, src_end = n0 >= 0 ? n0 : T.a1;
-  int js = j0, sc = j1 - j0;
-  while (js < j1) {
-    const int je = min(j1, js + sc);
-    const AtomFilter f{T.c, js, je, T.row_base, T.row_end, T.zv0, T.zv1};
-    int64_t pos = src_begin;
-    int n = build_list(p.supp, sh, src, pos, src_end, f);
-    if ((pos < src_end || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
-      sc = (sc + 1) >> 1;
-      continue;
-    }
-    // Candidates are consumed in ascending segments of <= stage_cap. More than
-    // one segment only happens for a single over-dense slab: later segments
-    // continue the per-voxel sums from the values this thread already stored.
-    bool first = true;
-    for (;;) {
-      // n == 0 still runs one pass: every slot is stored (as zero) exactly once
-      for (int s0 = 0; s0 < max(n, 1); s0 += p.stage_cap) {
-        const int ns = min(p.stage_cap, n - s0);
-        const int4* meta = sh.meta + s0;
-        // Stage gy (sub-chunk rows), gx (CTA rows) and gz (z window) of each candidate.
-        const int rows = T.row_end - T.row_base;
-        for (int q = warp; q < ns; q += nw) {
-          const int64_t a = meta[q].w;
-          float* dst = stage + q * p.stage_stride;
-          for (int e = lane; e < je - js; e += 32) dst[e] = __ldg(p.ty + a * p.ry + js + e);
-          for (int e = lane; e < rows; e += 32)
-            dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + T.row_base + e);
-          if (SW >= 4) {
-            const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz + T.zv0);
-            float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
-            for (int e = lane; e < zw * (SW / 4); e += 32) dst4[e] = __ldg(src4 + e);
-          } else {
-            for (int e = lane; e < T.zv1 - T.zv0; e += 32)
-              dst[p.stage_gz + e] = __ldg(p.tz + a * p.rz + T.zv0 + e);
-          }
-        }
-        // Warp-private ordered sublists: per row step m, the candidates whose
-        // x-support meets this warp's rows: {shared address of the block, slab mask}.
+  int c_lo = T.c, c_hi = T.c + 1;
+  if (p.fuse_channels) {
+    // Every channel from one candidate list and one staging pass, when the
+    // molecule's candidates for the whole chunk fit; otherwise the channels
+    // are served one after the other by the general path below.
+    c_lo = 0;
+    c_hi = p.C;
+    const AtomFilter fa{-1, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
+    int64_t pos = T.a0;
+    const int n = build_list(p.supp, sh, nullptr, pos, T.a1, fa);
+    if (pos >= T.a1 && n <= p.stage_cap) {
+      stage_tables<SW>(p, sh.meta, n, stage, j0, j1, T.row_base, rows, T.zv0, T.zv1);
+      __syncthreads();
+      float* out_b = p.out + T.b * p.C * chan_elems + j0 * p.slab_elems + slot0;
+      for (int c = 0; c < p.C; ++c) {
         Counts<M> cnt;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          const int rlo = T.row_base + T.wr0 + m * R, rhi = T.row_base + T.wr1 + m * R;
-          int filled = 0;
-          for (int q0 = 0; q0 < ns; q0 += 32) {
-            const int q = q0 + lane;
-            bool hit = false;
-            int2 ent = make_int2(0, 0);
-            if (q < ns) {
-              const int4 s = meta[q];
-              hit = lo16(s.x) <= rhi && hi16(s.x) > rlo;
-              const int lo = max(lo16(s.y), js) - js, hi = min(hi16(s.y), je) - js;
-              const unsigned long long mask = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
-              ent = make_int2((int)(stage_s + 4u * (unsigned)(q * p.stage_stride)),
-                              (int)(unsigned)mask);
-            }
-            const unsigned bal = __ballot_sync(kFull, hit);
-            if (hit) lists[m * p.stage_cap + filled + __popc(bal & ((1u << lane) - 1u))] = ent;
-            filled += __popc(bal);
-          }
-          cnt.v[m] = filled;
-        }
-        __syncthreads();  // staged tables visible to every warp (lists are warp-private)
-
-        if (first)
-          nz += accumulate_rows<M, SW, true>(out_c + js * p.slab_elems + slot0, p.slab_elems,
-                                              R * p.D, je - js, ibase, T.row_end, R, cnt, lists_s,
-                                              p.stage_cap, gx_off, gz_off, half);
-        else
-          nz += accumulate_rows<M, SW, false>(out_c + js * p.slab_elems + slot0, p.slab_elems,
-                                               R * p.D, je - js, ibase, T.row_end, R, cnt, lists_s,
-                                               p.stage_cap, gx_off, gz_off, half);
-        __syncthreads();  // the next segment / sub-chunk rewrites the staging area
-        first = false;
+        build_sublists<M>(p, sh.meta, n, c, lists, stage_s, j0, j1, rlo0, rhi0, R, cnt);
+        __syncwarp();
+        nz += accumulate_rows<M, SW, true>(out_b + c * chan_elems, p.slab_elems, R * p.D, j1 - j0,
+                                           ibase, T.row_end, R, cnt, lists_s, p.stage_cap, gx_off,
+                                           gz_off, half);
+        __syncwarp();   // the next channel rewrites this warp's sublists
       }
-      if (pos >= src_end) break;
-      n = build_list(p.supp, sh, src, pos, src_end, f);
+      c_hi = c_lo;   // done
     }
-    js = je;
+    __syncthreads();
+  }
+  for (int c = c_lo; c < c_hi; ++c) {
+    float* out_c = p.out + (T.b * p.C + c) * chan_elems;
+    // Level 0: the CTA's candidates over its whole chunk, scanned once from the
+    // molecule's atoms; sub-chunk lists below filter this short list instead.
+    // (skipped for small molecules: scanning them directly is as cheap)
+    const AtomFilter f0{c, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
+    const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x && p.c0_cap > 0
+                       ? build_index_list(p.supp, sh, c0, p.c0_cap, T.a0, T.a1, f0)
+                       : -1;
+    const int* src = n0 >= 0 ? c0 : nullptr;
+    const int64_t src_begin = n0 >= 0 ? 0 : T.a0, src_end = n0 >= 0 ? n0 : T.a1;
+    int js = j0, sc = j1 - j0;
+    while (js < j1) {
+      const int je = min(j1, js + sc);
+      const AtomFilter f{c, js, je, T.row_base, T.row_end, T.zv0, T.zv1};
+      int64_t pos = src_begin;
+      int n = build_list(p.supp, sh, src, pos, src_end, f);
+      if ((pos < src_end || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
+        sc = (sc + 1) >> 1;
+        continue;
+      }
+      // Candidates are consumed in ascending segments of <= stage_cap. More than
+      // one segment only happens for a single over-dense slab: later segments
+      // continue the per-voxel sums from the values this thread already stored.
+      bool first = true;
+      for (;;) {
+        // n == 0 still runs one pass: every slot is stored (as zero) exactly once
+        for (int s0 = 0; s0 < max(n, 1); s0 += p.stage_cap) {
+          const int ns = min(p.stage_cap, n - s0);
+          const int4* meta = sh.meta + s0;
+          stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
+          Counts<M> cnt;
+          build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, rlo0, rhi0, R, cnt);
+          __syncthreads();  // staged tables visible to every warp (lists are warp-private)
+
+          if (first)
+            nz += accumulate_rows<M, SW, true>(out_c + js * p.slab_elems + slot0, p.slab_elems,
+                                                R * p.D, je - js, ibase, T.row_end, R, cnt,
+                                                lists_s, p.stage_cap, gx_off, gz_off, half);
+          else
+            nz += accumulate_rows<M, SW, false>(out_c + js * p.slab_elems + slot0, p.slab_elems,
+                                                 R * p.D, je - js, ibase, T.row_end, R, cnt,
+                                                 lists_s, p.stage_cap, gx_off, gz_off, half);
+          __syncthreads();  // the next segment / sub-chunk rewrites the staging area
+          first = false;
+        }
+        if (pos >= src_end) break;
+        n = build_list(p.supp, sh, src, pos, src_end, f);
+      }
+      js = je;
+    }
   }
   if (p.stats != nullptr)
     finish_stats(p, sh, T.b, T.a0, T.a1, nz, T.c == 0 && chunk == 0 && rblk == 0 && zblk == 0);
@@ -1196,10 +1291,30 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int z_blocks = spr / zw;
   const int rows_per_cta = M * R < d.W ? M * R : d.W;
   const int64_t cta_bytes = (int64_t)rows_per_cta * zw * width * 4;
-  // y-slabs per CTA: aim for kTaskBytes of output (<= 32 for the slab masks)
-  int jc = (int)((kTaskBytes + cta_bytes - 1) / cta_bytes);
+  const int64_t mean_atoms = d.n_molecules > 0 ? (d.n_atoms + d.n_molecules - 1) / d.n_molecules : 0;
+  // Channel fusion (one CTA serves all C channels of its tile from one staged
+  // candidate list) for small molecules, whose whole atom list usually fits
+  // the staging area; VG_FUSE=0/1 overrides (tuning hook).
+  bool fuse = d.C > 1 && mean_atoms * 2 <= kStageCapMax;
+  if (const char* env = getenv("VG_FUSE")) fuse = d.C > 1 && env[0] == '1';
+  // Output bytes per CTA (measured on B200): fused CTAs ~1 MiB over all
+  // channels; per-channel CTAs 256 KiB, halved for dense molecules (hundreds
+  // of candidates per tile), whose shorter y-chunks halve less often.
+  int64_t task_bytes = fuse ? kFusedTaskBytes : (mean_atoms > 512 ? kTaskBytes / 2 : kTaskBytes);
+  // small batches: keep at least ~8 CTAs per SM in flight
+  const int64_t total_bytes = d.n_molecules * (int64_t)d.C * d.H * slab * 4;
+  if (task_bytes > total_bytes / kMinCtas) task_bytes = total_bytes / kMinCtas;
+  if (const char* env = getenv("VG_TASK_KB")) task_bytes = (int64_t)atoi(env) * 1024;
+  if (fuse) task_bytes = (task_bytes + d.C - 1) / d.C;   // per channel
+  // y-slabs per CTA: aim for task_bytes of output (<= 32 for the slab masks),
+  // then even out the chunks
+  int jc = (int)((task_bytes + cta_bytes - 1) / cta_bytes);
   jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
   if (jc > 32) jc = 32;
+  {
+    const int nch = (d.H + jc - 1) / jc;
+    jc = (d.H + nch - 1) / nch;
+  }
   p.jc = jc;
   p.n_jchunks = (d.H + jc - 1) / jc;
   if (d.C > 65535 || (int64_t)p.n_jchunks * row_blocks * z_blocks > 65535 ||
@@ -1216,7 +1331,6 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.stage_stride = p.stage_gz + round_up4(zw * width);
   // staging capacity: what the batch's molecules need (about 2x the mean atom
   // count), within the byte budget; small molecules keep CTAs small
-  const int64_t mean_atoms = d.n_molecules > 0 ? (d.n_atoms + d.n_molecules - 1) / d.n_molecules : 0;
   int cap = kStageBytes / (4 * p.stage_stride);
   const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > kStageCapMax ? kStageCapMax : mean_atoms * 2));
   if (cap > want) cap = want;
@@ -1229,7 +1343,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.stage_floats = (p.stage_cap * p.stage_stride + M * R + 8 + 3) & ~3;
   const size_t smem = (size_t)p.c0_cap * sizeof(int) + (size_t)p.stage_floats * sizeof(float) +
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
-  const dim3 grid((unsigned)d.n_molecules, (unsigned)d.C,
+  p.fuse_channels = fuse ? 1 : 0;
+  const dim3 grid((unsigned)d.n_molecules, fuse ? 1u : (unsigned)d.C,
                   (unsigned)(p.n_jchunks * row_blocks * z_blocks));
   if (sw == 8)
     launch_rows<8>(M, grid, nt, smem, st, p);
