@@ -1331,8 +1331,11 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.stage_stride = p.stage_gz + round_up4(zw * width);
   // staging capacity: what the batch's molecules need (about 2x the mean atom
   // count), within the byte budget; small molecules keep CTAs small
-  int cap = kStageBytes / (4 * p.stage_stride);
-  const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > kStageCapMax ? kStageCapMax : mean_atoms * 2));
+  int stage_bytes = kStageBytes, cap_max = kStageCapMax;
+  if (const char* env = getenv("VG_STAGE_KB")) stage_bytes = atoi(env) * 1024;
+  if (const char* env = getenv("VG_CAP_MAX")) cap_max = min(atoi(env), kListCap);
+  int cap = stage_bytes / (4 * p.stage_stride);
+  const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > cap_max ? cap_max : mean_atoms * 2));
   if (cap > want) cap = want;
   p.stage_cap = cap < 1 ? 1 : cap;
   // level-0 list only pays for large molecules (it is used when a molecule
