@@ -97,14 +97,14 @@ int vg_axis_tables_f32(const vg_batch_desc* desc, void* workspace, size_t worksp
 int vg_erf_f32(const float* t, float* out, int64_t n, void* stream);
 
 /* Grid reversal (reference reversal.py) building blocks.
- * vg_mse_f64 replaces _mse (reversal.py:226-228) for n_grids candidate grids
+ * vg_mse_f64 replaces _mse (reversal.py:256-258) for n_grids candidate grids
  * at once: out[g] = mean over n_voxels of (grids[g] - ref)^2 in fp64, fixed
  * reduction order (deterministic). Workspace: vg_mse_workspace_bytes(). */
 size_t vg_mse_workspace_bytes(int64_t n_voxels, int32_t n_grids);
 int vg_mse_f64(const float* ref, const float* grids, int64_t n_voxels, int32_t n_grids,
                double* out, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Replaces _gradient_from_diff / loss_gradient (reversal.py:240-289): grad
+/* Replaces _gradient_from_diff / loss_gradient (reversal.py:271-318): grad
  * [n_atoms*3] (x, y, z per atom, fp64) of mean((regen - ref)^2) w.r.t. the
  * atom coordinates of ONE molecule described by desc (open boundaries;
  * regen = the grid generated from desc, ref the target, both (C,H,W,D)). */

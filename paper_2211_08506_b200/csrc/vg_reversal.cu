@@ -3,10 +3,10 @@
 // The reversal (reference reversal.py) descends the grid-space MSE from seed
 // coordinates; every iteration regenerates candidate grids (the hot path,
 // vg_generate_f32) and needs
-//   * the loss  _mse (reversal.py:226-228): mean((regen - ref)^2) in fp64 —
+//   * the loss  _mse (reversal.py:256-258): mean((regen - ref)^2) in fp64 —
 //     vg_mse_f64 does G candidate grids at once, two-pass fixed-order
 //     reduction (deterministic);
-//   * the analytic gradient _gradient_from_diff (reversal.py:240-276):
+//   * the analytic gradient _gradient_from_diff (reversal.py:271-306):
 //     per atom and axis, 2/N * sum over the support block of
 //     (regen - ref) * f_x[i] f_y[j] f_z[k] in fp64, where the axis' factor is
 //     the derivative table (axis_gradient, kernels.py:277-296, built on
@@ -14,7 +14,7 @@
 //     tables — vg_loss_gradient_f64, one CTA per atom, tables in shared memory.
 // Bits follow the reference where it matters for the path (value tables are
 // the K1 numerics); the fp64 sums and float32 expm1 of the derivative are
-// tolerance-level.
+// tolerance-level (row f2).
 
 #include <cuda_runtime.h>
 
