@@ -25,7 +25,7 @@ extern "C" {
 #define VG_ERR_CUDA -2      /* a CUDA launch or runtime call failed             */
 #define VG_ERR_WORKSPACE -3 /* workspace pointer NULL or too small              */
 
-#define VG_ABI_VERSION 1
+#define VG_ABI_VERSION 2
 
 /* One batch of molecules in CSR form plus the grid geometry.
  *
@@ -67,6 +67,12 @@ typedef struct vg_mol_stats {
 typedef struct vg_ws_layout {
   size_t tx, ty, tz, supp, total;
   int32_t row_x, row_y, row_z;
+  /* K3 candidate bins (large molecules only; bin_jc == 0 when unused):
+   * ordered atom indices per (molecule, channel, y-chunk of bin_jc slabs)
+   * at `bins`, per-molecule bin offsets at `bin_off`. Scratch written by
+   * vg_generate_f32 / vg_slabs_f32. */
+  size_t bins, bin_off;
+  int32_t bin_jc, bin_chunks;
 } vg_ws_layout;
 
 /* Workspace needed by vg_generate_f32 / vg_axis_tables_f32. */
@@ -84,7 +90,7 @@ int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspace,
  * tables already computed into `workspace` by vg_axis_tables_f32 for the same
  * descriptor (stream-ordered). Lets a caller time the slab kernel by itself or
  * regenerate grids from cached tables. */
-int vg_slabs_f32(const vg_batch_desc* desc, float* out, const void* workspace,
+int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
                  size_t workspace_bytes, vg_mol_stats* stats, void* stream);
 
 /* Replaces fused_axis_tables (kernels.py:217-274) for every atom of the

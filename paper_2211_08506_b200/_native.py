@@ -66,6 +66,10 @@ class VgWsLayout(ctypes.Structure):
         ("row_x", ctypes.c_int32),
         ("row_y", ctypes.c_int32),
         ("row_z", ctypes.c_int32),
+        ("bins", ctypes.c_size_t),
+        ("bin_off", ctypes.c_size_t),
+        ("bin_jc", ctypes.c_int32),
+        ("bin_chunks", ctypes.c_int32),
     ]
 
 
@@ -96,7 +100,7 @@ SIGNATURES = {
     "vg_abi_version": (ctypes.c_int, []),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 _lib = None
 
 

@@ -82,6 +82,8 @@ constexpr int kStageCapMax = 96;     // K3: staged candidates per sub-chunk (upp
 constexpr int64_t kTaskBytes = 262144;       // K3: output bytes per CTA (y-chunk sizing)
 constexpr int64_t kFusedTaskBytes = 1048576; // ... per channel-fused CTA, all channels
 constexpr int64_t kMinCtas = 148 * 8;         // K3: CTAs a launch should at least offer
+constexpr int kMaxBins = 2048;                // K2: bins (channels x y-chunks) per molecule
+constexpr int kBinWarps = 8;                  // K2: warps per molecule CTA
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -366,6 +368,18 @@ struct SlabParams {
   int stage_floats;     // floats of the staging area (sublists follow it)
   int c0_cap;           // level-0 candidate capacity (ints before the staging area)
   int fuse_channels;    // 1: one CTA serves every channel (grid.y == 1)
+  // K2 candidate bins (NULL: scan the molecule's atoms)
+  const int* bins;      // molecule b's bins start at bins + offsets[b] * n_jchunks
+  const int* bin_off;   // [B][bin_nb + 1] offsets into the molecule's bins
+  int bin_nb;           // C * n_jchunks
+};
+
+struct BinParams {
+  const int64_t* offsets;
+  const int4* supp;
+  int* bins;
+  int* bin_off;
+  int nb, nch, jc;
 };
 
 struct SlabShared {
@@ -446,6 +460,28 @@ __device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t
                           int c, int jlo, int jhi, int xa, int xb) {
   const AtomFilter f{c, jlo, jhi, xa, xb, 0, kMaxAxis};
   return build_list(supp, sh, nullptr, pos, a1, f);
+}
+
+// Ordered compaction into c0 of the atoms listed in src[0, n) that pass f
+// (a K2 bin). Returns the count, or -1 if more than cap atoms pass.
+__device__ int build_index_list(const int4* __restrict__ supp, SlabShared& sh, int* c0, int cap,
+                                const int* __restrict__ src, int n, const AtomFilter& f) {
+  int count = 0;
+  for (int pos = 0; pos < n; pos += blockDim.x) {
+    const int p = pos + threadIdx.x;
+    int atom = 0;
+    bool keep = false;
+    if (p < n) {
+      atom = __ldg(src + p);
+      keep = f(__ldg(supp + atom));
+    }
+    int total;
+    const int rank = block_rank(keep, sh.warp_cnt, total);
+    if (keep && count + rank < cap) c0[count + rank] = atom;
+    count += total;
+    __syncthreads();
+  }
+  return count <= cap ? count : -1;
 }
 
 // Ordered compaction of atom indices into c0 (the CTA's level-0
@@ -782,15 +818,21 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
       float* dst = dst_j + m * m_stride;
       Slot acc;
       zero_slot(acc);
+      int before = 0;
       if (!FIRST && mine) {
         ld_slot(acc, dst, half);
-        nz -= nonzeros_pos(acc);
+        before = nonzeros_pos(acc);
       }
       const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
+      // touched (warp-uniform): some candidate was active on this slab and
+      // step; untouched slots keep their value, so their count is unchanged
+      bool touched;
       if (small) {
-        walk_group(__ballot_sync(kFull, (pre[m].y & jbit) != 0), pre[m].x, gy_off, gxm, gz_off,
-                   halfb, acc);
+        const unsigned act = __ballot_sync(kFull, (pre[m].y & jbit) != 0);
+        touched = act != 0u;
+        walk_group(act, pre[m].x, gy_off, gxm, gz_off, halfb, acc);
       } else {
+        touched = false;
         // 32 entries at a time: each lane tests one entry's slab mask, the
         // ballot gives the entries active on this slab, visited in ascending
         // order (ascending atom order) with no cost for the inactive ones.
@@ -799,38 +841,62 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
           const int e = c0 + lane;
           int2 ent = make_int2(0, 0);
           if (e < cnt.v[m]) ent = lds_int2(L + 8u * (unsigned)e);
-          walk_group(__ballot_sync(kFull, (ent.y & jbit) != 0), ent.x, gy_off, gxm, gz_off, halfb,
-                     acc);
+          const unsigned act = __ballot_sync(kFull, (ent.y & jbit) != 0);
+          touched = touched || act != 0u;
+          walk_group(act, ent.x, gy_off, gxm, gz_off, halfb, acc);
         }
       }
       if (mine) {
         st_slot(dst, acc, half);
-        if (!FIRST || cnt.v[m] != 0) nz += nonzeros_pos(acc);
+        if (touched) nz += nonzeros_pos(acc) - before;
       }
     }
   }
   return nz;
 }
 
+// Asynchronous global -> shared copies (LDGSTS): a warp issues every copy of
+// its candidates back to back instead of waiting on each load; completion is
+// awaited once (cp_async_wait_all) before the barrier that publishes them.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Stage gy (slabs js..je), gx (CTA rows) and gz (z window) of candidates
 // meta[0..ns) into consecutive blocks of the staging area, one warp per block.
+// The copies are asynchronous: call cp_async_wait_all() before the barrier.
 template <int SW>
 __device__ __forceinline__ void stage_tables(const SlabParams& p, const int4* meta, int ns,
                                              float* stage, int js, int je, int row_base, int rows,
                                              int zv0, int zv1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool gx16 = (row_base & 3) == 0;   // table rows are 16-byte aligned (pad4)
+  const int rows4 = (rows + 3) >> 2;
   for (int q = warp; q < ns; q += nw) {
     const int64_t a = meta[q].w;
     float* dst = stage + q * p.stage_stride;
-    for (int e = lane; e < je - js; e += 32) dst[e] = __ldg(p.ty + a * p.ry + js + e);
-    for (int e = lane; e < rows; e += 32)
-      dst[p.stage_gx + e] = __ldg(p.tx + a * p.rx + row_base + e);
-    if (SW >= 4) {
-      const float4* src4 = reinterpret_cast<const float4*>(p.tz + a * p.rz + zv0);
-      float4* dst4 = reinterpret_cast<float4*>(dst + p.stage_gz);
-      for (int e = lane; e < p.zw * (SW / 4); e += 32) dst4[e] = __ldg(src4 + e);
+    for (int e = lane; e < je - js; e += 32) cp_async4(dst + e, p.ty + a * p.ry + js + e);
+    const float* gx = p.tx + a * p.rx + row_base;
+    if (gx16) {
+      for (int e = lane; e < rows4; e += 32) cp_async16(dst + p.stage_gx + 4 * e, gx + 4 * e);
     } else {
-      for (int e = lane; e < zv1 - zv0; e += 32) dst[p.stage_gz + e] = __ldg(p.tz + a * p.rz + zv0 + e);
+      for (int e = lane; e < rows; e += 32) cp_async4(dst + p.stage_gx + e, gx + e);
+    }
+    if (SW >= 4) {
+      const float* gz = p.tz + a * p.rz + zv0;
+      for (int e = lane; e < p.zw * (SW / 4); e += 32)
+        cp_async16(dst + p.stage_gz + 4 * e, gz + 4 * e);
+    } else {
+      for (int e = lane; e < zv1 - zv0; e += 32)
+        cp_async4(dst + p.stage_gz + e, p.tz + a * p.rz + zv0 + e);
     }
   }
 }
@@ -932,6 +998,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
     const int n = build_list(p.supp, sh, nullptr, pos, T.a1, fa);
     if (pos >= T.a1 && n <= p.stage_cap) {
       stage_tables<SW>(p, sh.meta, n, stage, j0, j1, T.row_base, rows, T.zv0, T.zv1);
+      cp_async_wait_all();
       __syncthreads();
       float* out_b = p.out + T.b * p.C * chan_elems + j0 * p.slab_elems + slot0;
       for (int c = 0; c < p.C; ++c) {
@@ -953,11 +1020,27 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
     // molecule's atoms; sub-chunk lists below filter this short list instead.
     // (skipped for small molecules: scanning them directly is as cheap)
     const AtomFilter f0{c, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
-    const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x && p.c0_cap > 0
-                       ? build_index_list(p.supp, sh, c0, p.c0_cap, T.a0, T.a1, f0)
-                       : -1;
-    const int* src = n0 >= 0 ? c0 : nullptr;
-    const int64_t src_begin = n0 >= 0 ? 0 : T.a0, src_end = n0 >= 0 ? n0 : T.a1;
+    const int* src;
+    int64_t src_begin, src_end;
+    if (p.bins != nullptr) {
+      // K2 bin of (molecule, channel, y-chunk): already ordered and y-culled
+      const int* bo = p.bin_off + T.b * (p.bin_nb + 1) + c * p.n_jchunks + chunk;
+      const int q0 = __ldg(bo), nbk = __ldg(bo + 1) - q0;
+      const int* bl = p.bins + T.a0 * p.n_jchunks + q0;
+      const int n0 = nbk > 2 * (int)blockDim.x && p.c0_cap > 0
+                         ? build_index_list(p.supp, sh, c0, p.c0_cap, bl, nbk, f0)
+                         : -1;
+      src = n0 >= 0 ? c0 : bl;
+      src_begin = 0;
+      src_end = n0 >= 0 ? n0 : nbk;
+    } else {
+      const int n0 = T.a1 - T.a0 > 2 * (int64_t)blockDim.x && p.c0_cap > 0
+                         ? build_index_list(p.supp, sh, c0, p.c0_cap, T.a0, T.a1, f0)
+                         : -1;
+      src = n0 >= 0 ? c0 : nullptr;
+      src_begin = n0 >= 0 ? 0 : T.a0;
+      src_end = n0 >= 0 ? n0 : T.a1;
+    }
     int js = j0, sc = j1 - j0;
     while (js < j1) {
       const int je = min(j1, js + sc);
@@ -980,6 +1063,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
           stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
           Counts<M> cnt;
           build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, rlo0, rhi0, R, cnt);
+          cp_async_wait_all();
           __syncthreads();  // staged tables visible to every warp (lists are warp-private)
 
           if (first)
@@ -1001,6 +1085,102 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   }
   if (p.stats != nullptr)
     finish_stats(p, sh, T.b, T.a0, T.a1, nz, T.c == 0 && chunk == 0 && rblk == 0 && zblk == 0);
+}
+
+// ---------------------------------------------------------------------------
+// K2: ordered candidate bins for large molecules
+// ---------------------------------------------------------------------------
+// One CTA per molecule. Bin q = channel * nch + y-chunk holds, in ascending
+// atom order, every atom of that channel with a non-empty support box whose
+// y-support meets the chunk [k*jc, (k+1)*jc). Warp w owns a contiguous atom
+// range; per-warp counts, a prefix over warps and bins, then an ordered fill
+// (ranks within a warp from __match_any_sync) keep the order deterministic
+// without sorting. K3's per-channel CTAs then scan their bin instead of the
+// whole molecule.
+__device__ __forceinline__ void bin_range(const BinParams& p, const int4& s, int jc, bool valid,
+                                          bool& member, int& c, int& k0, int& k1) {
+  member = valid && lo16(s.x) < hi16(s.x) && lo16(s.y) < hi16(s.y) && lo16(s.z) < hi16(s.z);
+  c = s.w;
+  k0 = member ? lo16(s.y) / jc : 0;
+  k1 = member ? (hi16(s.y) - 1) / jc : -1;
+}
+
+__global__ void __launch_bounds__(kBinWarps * 32) vg_bin_kernel(const __grid_constant__ BinParams p) {
+  extern __shared__ int bsm[];
+  int* cnt = bsm;                      // [kBinWarps][nb]: counts, then write cursors
+  int* start = bsm + kBinWarps * p.nb; // [nb]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = blockIdx.x;
+  const int64_t a0 = __ldg(p.offsets + b), a1 = __ldg(p.offsets + b + 1);
+  const int nb = p.nb, nch = p.nch;
+  for (int i = threadIdx.x; i < kBinWarps * nb; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const int64_t n = a1 - a0;
+  const int64_t per = ((n + kBinWarps - 1) / kBinWarps + 31) / 32 * 32;
+  const int64_t w0 = a0 + warp * per, w1 = min(a1, w0 + per);
+  int* mine = cnt + warp * nb;
+  int* out = p.bins + a0 * nch;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int64_t g = w0; g < w1; g += 32) {
+      const int64_t a = g + lane;
+      const bool valid = a < w1;
+      const int4 s = valid ? __ldg(p.supp + a) : make_int4(0, 0, 0, 0);
+      bool member;
+      int c, k0, k1;
+      bin_range(p, s, p.jc, valid, member, c, k0, k1);
+      const int kmin = __reduce_min_sync(kFull, member ? k0 : INT_MAX);
+      const int kmax = __reduce_max_sync(kFull, member ? k1 : -1);
+      for (int k = kmin; k <= kmax; ++k) {
+        const bool in = member && k0 <= k && k <= k1;
+        const int q = in ? c * nch + k : -1;
+        const unsigned peers = __match_any_sync(kFull, q);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (in && lane == leader) base = mine[q];
+        base = __shfl_sync(kFull, base, leader);
+        if (in) {
+          if (pass == 1) out[base + __popc(peers & ((1u << lane) - 1u))] = (int)a;
+          if (lane == leader) mine[q] = base + __popc(peers);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (pass == 0) {
+      // per bin: exclusive prefix over warps (then the bin's total)
+      for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+        int run = 0;
+        for (int w = 0; w < kBinWarps; ++w) {
+          const int v = cnt[w * nb + q];
+          cnt[w * nb + q] = run;
+          run += v;
+        }
+        start[q] = run;
+      }
+      __syncthreads();
+      // exclusive scan of bin totals (one warp, 32 bins per step)
+      if (warp == 0) {
+        int carry = 0;
+        for (int q0 = 0; q0 < nb; q0 += 32) {
+          const int q = q0 + lane;
+          const int v = q < nb ? start[q] : 0;
+          int x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+          }
+          if (q < nb) start[q] = carry + x - v;
+          carry += __shfl_sync(kFull, x, 31);
+        }
+        if (lane == 0) p.bin_off[b * (nb + 1) + nb] = carry;
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < nb; q += blockDim.x) p.bin_off[b * (nb + 1) + q] = start[q];
+      for (int i = threadIdx.x; i < kBinWarps * nb; i += blockDim.x) cnt[i] += start[i % nb];
+      __syncthreads();
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1049,6 +1229,10 @@ int validate(const vg_batch_desc* d) {
   return VG_OK;
 }
 
+// y-chunking of the candidate bins (K2) for this batch, or false if K3 will
+// not use bins (defined with the K3 launch plan below).
+bool bin_plan(const vg_batch_desc& d, int* jc, int* nch);
+
 void fill_layout(const vg_batch_desc* d, vg_ws_layout* L) {
   const size_t na = (size_t)d->n_atoms;
   L->row_x = round_up4(d->W);
@@ -1063,6 +1247,20 @@ void fill_layout(const vg_batch_desc* d, vg_ws_layout* L) {
   off = align_up(off + na * L->row_z * sizeof(float), 256);
   L->supp = off;
   off = align_up(off + na * 4 * sizeof(int32_t), 256);
+  // candidate bins: atom indices, molecule b's region holds (atoms of b) x
+  // chunks entries from offsets[b] * chunks; then per molecule C*chunks+1
+  // bin offsets
+  int jc = 0, nch = 0;
+  L->bins = L->bin_off = 0;
+  L->bin_jc = L->bin_chunks = 0;
+  if (bin_plan(*d, &jc, &nch)) {
+    L->bin_jc = jc;
+    L->bin_chunks = nch;
+    L->bins = off;
+    off = align_up(off + na * (size_t)nch * sizeof(int32_t), 256);
+    L->bin_off = off;
+    off = align_up(off + (size_t)d->n_molecules * ((size_t)d->C * nch + 1) * sizeof(int32_t), 256);
+  }
   L->total = off == 0 ? 256 : off;
 }
 
@@ -1148,7 +1346,9 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   const int base = spr / gcd_int(32, spr) * 32;  // lcm(32, spr)
   if (base > kRowThreads) return false;
   double best = 1e30;
+  const char* fq = getenv("VG_PLAN_Q");   // tuning hook: force the thread multiple
   for (int q = 1; base * q <= kRowThreads; ++q) {
+    if (fq != nullptr && atoi(fq) != q) continue;
     const int t = base * q, r = t / spr;
     const int need = (W + r - 1) / r;
     int m = need < 8 ? need : 8;
@@ -1225,19 +1425,97 @@ int pick_sw(int D, bool aligned16) {
 }
 
 // K3 launch (tables must already be in the workspace, same stream).
+// K3 launch plan, shared by the workspace layout (which sizes the candidate
+// bins for the plan's y-chunks) and the launch.
+struct SlabPlan {
+  bool rows_ok;         // row-structured kernel (else the generic one)
+  bool vec;             // generic kernel: float4 slots
+  int sw, width, spr, zw;
+  int nt, R, M, row_blocks, z_blocks;
+  int jc, n_jchunks;
+  bool fuse;
+  int64_t mean_atoms;
+};
+
+void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
+  memset(P, 0, sizeof *P);
+  P->sw = pick_sw(d.D, aligned16);
+  const int64_t slab = (int64_t)d.W * d.D;
+  const char* force = getenv("VG_FORCE_GENERIC");
+  P->zw = pick_zw(d.D / P->sw, P->sw);
+  P->rows_ok = !(force && force[0] == '1') &&
+               plan_rows(P->zw, d.W, &P->nt, &P->R, &P->M, &P->row_blocks);
+  // the generic kernel works in float4 or float slots
+  P->vec = P->rows_ok ? P->sw >= 4 : (d.D % 4 == 0 && aligned16);
+  P->width = P->rows_ok ? P->sw : (P->vec ? 4 : 1);
+  P->spr = d.D / P->width;
+  P->mean_atoms = d.n_molecules > 0 ? (d.n_atoms + d.n_molecules - 1) / d.n_molecules : 0;
+  if (!P->rows_ok) return;
+  P->z_blocks = P->spr / P->zw;
+  const int rows_per_cta = P->M * P->R < d.W ? P->M * P->R : d.W;
+  const int64_t cta_bytes = (int64_t)rows_per_cta * P->zw * P->width * 4;
+  const int64_t mean_atoms = P->mean_atoms;
+  // Channel fusion (one CTA serves all C channels of its tile from one staged
+  // candidate list) for small molecules, whose whole atom list usually fits
+  // the staging area; VG_FUSE=0/1 overrides (tuning hook).
+  bool fuse = d.C > 1 && mean_atoms * 2 <= kStageCapMax;
+  if (const char* env = getenv("VG_FUSE")) fuse = d.C > 1 && env[0] == '1';
+  // Output bytes per CTA (measured on B200): fused CTAs ~1 MiB over all
+  // channels; per-channel CTAs 256 KiB, halved for dense molecules (hundreds
+  // of candidates per tile), whose shorter y-chunks halve less often.
+  int64_t task_bytes = fuse ? kFusedTaskBytes : (mean_atoms > 512 ? kTaskBytes / 2 : kTaskBytes);
+  // small batches: keep at least ~8 CTAs per SM in flight
+  const int64_t total_bytes = d.n_molecules * (int64_t)d.C * d.H * slab * 4;
+  if (task_bytes > total_bytes / kMinCtas) task_bytes = total_bytes / kMinCtas;
+  if (const char* env = getenv("VG_TASK_KB")) task_bytes = (int64_t)atoi(env) * 1024;
+  if (fuse) task_bytes = (task_bytes + d.C - 1) / d.C;   // per channel
+  // y-slabs per CTA: aim for task_bytes of output (<= 32 for the slab masks),
+  // then even out the chunks
+  int jc = (int)((task_bytes + cta_bytes - 1) / cta_bytes);
+  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
+  if (jc > 32) jc = 32;
+  {
+    const int nch = (d.H + jc - 1) / jc;
+    jc = (d.H + nch - 1) / nch;
+  }
+  P->jc = jc;
+  P->n_jchunks = (d.H + jc - 1) / jc;
+  P->fuse = fuse;
+}
+
+// Candidate bins (K2) pay for molecules large enough that every CTA would
+// otherwise scan thousands of atoms: per-channel CTAs, > 2*256 atoms on
+// average, and a bounded number of bins per molecule.
+bool want_bins(const vg_batch_desc& d, const SlabPlan& P) {
+  if (const char* env = getenv("VG_BINS")) {
+    if (env[0] == '0') return false;
+  }
+  if (!P.rows_ok || P.fuse || d.periodic) return false;
+  if (P.mean_atoms <= 2 * kRowThreads) return false;
+  const int64_t nb = (int64_t)d.C * P.n_jchunks;
+  return nb <= kMaxBins && (int64_t)d.n_atoms * P.n_jchunks <= (int64_t)1 << 28;
+}
+
+bool bin_plan(const vg_batch_desc& d, int* jc, int* nch) {
+  if (d.n_molecules == 0 || d.n_atoms == 0) return false;
+  SlabPlan P;
+  plan_slabs(d, true, &P);   // outputs from the torch allocator are 16-byte aligned
+  if (!want_bins(d, P)) return false;
+  *jc = P.jc;
+  *nch = P.n_jchunks;
+  return true;
+}
+
+// K3 launch (tables must already be in the workspace, same stream).
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
                  vg_mol_stats* stats, cudaStream_t st) {
   const bool aligned16 = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  const int sw = pick_sw(d.D, aligned16);
+  SlabPlan P;
+  plan_slabs(d, aligned16, &P);
   const int64_t slab = (int64_t)d.W * d.D;
-  const char* force = getenv("VG_FORCE_GENERIC");
-  const int zw = pick_zw(d.D / sw, sw);
-  int nt = 0, R = 0, M = 0, row_blocks = 0;
-  const bool rows_ok = !(force && force[0] == '1') && plan_rows(zw, d.W, &nt, &R, &M, &row_blocks);
-  // the generic kernel works in float4 or float slots
-  const bool vec = rows_ok ? sw >= 4 : (d.D % 4 == 0 && aligned16);
-  const int width = rows_ok ? sw : (vec ? 4 : 1);
-  const int spr = d.D / width;
+  const int sw = P.sw, zw = P.zw, width = P.width, spr = P.spr;
+  int nt = P.nt;
+  const int R = P.R, M = P.M, row_blocks = P.row_blocks;
 
   SlabParams p;
   memset(&p, 0, sizeof p);
@@ -1263,7 +1541,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
   }
 
-  if (!rows_ok) {
+  if (!P.rows_ok) {
+    const bool vec = P.vec;
     const int64_t nslots64 = slab / width;
     if (nslots64 > INT_MAX / 2) return set_error(VG_ERR_INVALID, "slab W*D too large");
     const int nslots = (int)nslots64;
@@ -1288,38 +1567,41 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     return check_launch("vg_slab_generic_kernel");
   }
 
-  const int z_blocks = spr / zw;
-  const int rows_per_cta = M * R < d.W ? M * R : d.W;
-  const int64_t cta_bytes = (int64_t)rows_per_cta * zw * width * 4;
-  const int64_t mean_atoms = d.n_molecules > 0 ? (d.n_atoms + d.n_molecules - 1) / d.n_molecules : 0;
-  // Channel fusion (one CTA serves all C channels of its tile from one staged
-  // candidate list) for small molecules, whose whole atom list usually fits
-  // the staging area; VG_FUSE=0/1 overrides (tuning hook).
-  bool fuse = d.C > 1 && mean_atoms * 2 <= kStageCapMax;
-  if (const char* env = getenv("VG_FUSE")) fuse = d.C > 1 && env[0] == '1';
-  // Output bytes per CTA (measured on B200): fused CTAs ~1 MiB over all
-  // channels; per-channel CTAs 256 KiB, halved for dense molecules (hundreds
-  // of candidates per tile), whose shorter y-chunks halve less often.
-  int64_t task_bytes = fuse ? kFusedTaskBytes : (mean_atoms > 512 ? kTaskBytes / 2 : kTaskBytes);
-  // small batches: keep at least ~8 CTAs per SM in flight
-  const int64_t total_bytes = d.n_molecules * (int64_t)d.C * d.H * slab * 4;
-  if (task_bytes > total_bytes / kMinCtas) task_bytes = total_bytes / kMinCtas;
-  if (const char* env = getenv("VG_TASK_KB")) task_bytes = (int64_t)atoi(env) * 1024;
-  if (fuse) task_bytes = (task_bytes + d.C - 1) / d.C;   // per channel
-  // y-slabs per CTA: aim for task_bytes of output (<= 32 for the slab masks),
-  // then even out the chunks
-  int jc = (int)((task_bytes + cta_bytes - 1) / cta_bytes);
-  jc = jc < 1 ? 1 : (jc > d.H ? d.H : jc);
-  if (jc > 32) jc = 32;
-  {
-    const int nch = (d.H + jc - 1) / jc;
-    jc = (d.H + nch - 1) / nch;
-  }
+  const int z_blocks = P.z_blocks;
+  const int64_t mean_atoms = P.mean_atoms;
+  const bool fuse = P.fuse;
+  const int jc = P.jc;
   p.jc = jc;
-  p.n_jchunks = (d.H + jc - 1) / jc;
+  p.n_jchunks = P.n_jchunks;
   if (d.C > 65535 || (int64_t)p.n_jchunks * row_blocks * z_blocks > 65535 ||
       d.n_molecules > INT_MAX)
     return set_error(VG_ERR_INVALID, "grid too large for the slab kernel");
+  // K2: ordered per-(molecule, channel, y-chunk) candidate bins, when the
+  // workspace was laid out for this plan's chunks
+  if (L.bin_jc == jc && L.bin_chunks == p.n_jchunks && L.bin_jc > 0) {
+    const int nb = d.C * p.n_jchunks;
+    p.bins = reinterpret_cast<int*>(ws + L.bins);
+    p.bin_off = reinterpret_cast<int*>(ws + L.bin_off);
+    p.bin_nb = nb;
+    BinParams bp;
+    bp.offsets = d.offsets;
+    bp.supp = p.supp;
+    bp.bins = reinterpret_cast<int*>(ws + L.bins);
+    bp.bin_off = reinterpret_cast<int*>(ws + L.bin_off);
+    bp.nb = nb;
+    bp.nch = p.n_jchunks;
+    bp.jc = jc;
+    const size_t bsmem = (size_t)(kBinWarps + 1) * nb * sizeof(int);
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(vg_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (kBinWarps + 1) * kMaxBins * (int)sizeof(int));
+      configured = true;
+    }
+    vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
+    const int rc = check_launch("vg_bin_kernel");
+    if (rc != VG_OK) return rc;
+  }
   p.row_blocks = row_blocks;
   p.z_blocks = z_blocks;
   p.zw = zw;
@@ -1385,12 +1667,12 @@ VG_API int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspac
   return launch_slabs(*desc, L, ws, out, stats, st);
 }
 
-VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, const void* workspace,
+VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
                         size_t workspace_bytes, vg_mol_stats* stats, void* stream) {
   vg_ws_layout L;
-  int rc = prepare(desc, out, const_cast<void*>(workspace), workspace_bytes, &L);
+  int rc = prepare(desc, out, workspace, workspace_bytes, &L);
   if (rc != VG_OK || desc->n_molecules == 0) return rc;
-  return launch_slabs(*desc, L, static_cast<char*>(const_cast<void*>(workspace)), out, stats,
+  return launch_slabs(*desc, L, static_cast<char*>(workspace), out, stats,
                       static_cast<cudaStream_t>(stream));
 }
 

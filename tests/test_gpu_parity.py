@@ -362,6 +362,36 @@ def test_candidate_list_overflow_path_vs_oracle():
     assert int(st[0, 0]) == rs["voxel_writes"] and int(st[0, 1]) == rs["nonzero_voxels"]
 
 
+@pytest.mark.parametrize("policy", ["fixed", "per-molecule-bbox"])
+def test_candidate_bins_vs_oracle_and_unbinned(policy, monkeypatch):
+    """K2 bins (large molecules): mixed sizes incl. empty and tiny molecules,
+    atoms outside the box, 3 channels, odd shape; equal to the oracle and to
+    the unbinned scan path (VG_BINS=0)."""
+    rng = np.random.default_rng(17)
+    sizes = [1400, 0, 3, 900, 2100, 700]
+    sets = []
+    for n in sizes:
+        xyz = rng.normal(6.0, 2.5, size=(n, 3))
+        sets.append(vg.ParticleSet(rng.integers(0, 3, size=n), xyz))
+    spec = vg.GridSpec((37, 30, 44), 3, vg.BoundingBox((0, 0, 0), (12, 12, 12)), 0.45)
+    got = vg.generate_batch(sets, spec, spec_policy=policy)
+    monkeypatch.setenv("VG_BINS", "0")
+    plain = vg.generate_batch(sets, spec, spec_policy=policy)
+    monkeypatch.delenv("VG_BINS")
+    a, b = got.tensor.cpu().numpy(), plain.tensor.cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert plain.errors.keys() == got.errors.keys()
+    for i, ps in enumerate(sets):
+        if i in got.errors:
+            continue
+        g, st = got.results[i]
+        sp = g.spec
+        ref, rs = orc.grid(np.asarray(ps.channels), np.asarray(ps.positions),
+                           orc.Geometry(sp.shape, 3, sp.box.origin, sp.box.extents, 0.45))
+        assert_bitwise(a[i], ref, f"bins {policy} {i}")
+        assert st.voxel_writes == rs["voxel_writes"] and st.nonzero_voxels == rs["nonzero_voxels"]
+
+
 @pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 7), (5, 3, 4), (33, 31, 36), (4, 70, 8)])
 def test_odd_shapes_vs_oracle(shape):
     rng = np.random.default_rng(sum(shape))
