@@ -65,7 +65,10 @@ int check_launch(const char* what) {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
-constexpr int kListCap = 128;        // K3: candidate segment capacity (>= kStageCapMax)
+#ifndef VG_LIST_CAP
+#define VG_LIST_CAP 128
+#endif
+constexpr int kListCap = VG_LIST_CAP;  // K3: candidate segment capacity (staged candidates max)
 constexpr int kC0CapMax = 1536;      // K3 row kernel: level-0 candidates kept per CTA (max)
 constexpr int kMaxCtaRows = 64;      // K3 row kernel: x rows per CTA (keeps staged rows short)
 constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
@@ -77,8 +80,6 @@ constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bou
 #define VG_ROW_MINB1 VG_ROW_MINB   // ... for one row step per CTA (M = 1)
 #endif
 constexpr int row_minb(int m) { return m == 1 ? VG_ROW_MINB1 : VG_ROW_MINB; }
-constexpr int kStageBytes = 24576;   // K3: shared-memory staging budget per CTA
-constexpr int kStageCapMax = 96;     // K3: staged candidates per sub-chunk (upper bound)
 constexpr int64_t kTaskBytes = 262144;       // K3: output bytes per CTA (y-chunk sizing)
 constexpr int64_t kFusedTaskBytes = 1048576; // ... per channel-fused CTA, all channels
 constexpr int64_t kMinCtas = 148 * 8;         // K3: CTAs a launch should at least offer
@@ -368,6 +369,8 @@ struct SlabParams {
   int stage_floats;     // floats of the staging area (sublists follow it)
   int c0_cap;           // level-0 candidate capacity (ints before the staging area)
   int fuse_channels;    // 1: one CTA serves every channel (grid.y == 1)
+  int gx_win;           // staged gx rows per candidate (window), 0: all CTA rows
+  int gx_wmax;          // rows one warp spans in a row step (window padding)
   // K2 candidate bins (NULL: scan the molecule's atoms)
   const int* bins;      // molecule b's bins start at bins + offsets[b] * n_jchunks
   const int* bin_off;   // [B][bin_nb + 1] offsets into the molecule's bins
@@ -759,10 +762,14 @@ __device__ __forceinline__ void lds_slot2(Slot8& v, unsigned a, unsigned halfb) 
 
 // One candidate term: ((gy*gx)*gz) added to the slot (kernels' op order).
 template <typename Slot>
-__device__ __forceinline__ void term_of(unsigned blk, unsigned gy_off, unsigned gxm, unsigned gz_off,
+__device__ __forceinline__ void term_of(unsigned ent, unsigned gy_off, unsigned gxm, unsigned gz_off,
                                         unsigned halfb, Slot& gz, float& pyx) {
+  // entry: shared address of the block (low 24 bits) | first staged x row
+  // relative to the CTA's rows (high 8 bits, windowed gx staging)
+  const unsigned blk = ent & 0xFFFFFFu;
+  const unsigned gxb = blk - ((ent >> 24) << 2);
   lds_slot2(gz, blk + gz_off, halfb);
-  pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(blk + gxm));  // ty (x) tx
+  pyx = VG_FMUL(lds_f32(blk + gy_off), lds_f32(gxb + gxm));  // ty (x) tx
 }
 
 // Walk the active entries `act` (ballot over a 32-entry group, ascending =
@@ -870,6 +877,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// First staged x row of a candidate under windowed gx staging: every warp
+// whose rows meet the x-support [xlo, xhi) reads rows within
+// [xlo - (wmax-1), xhi + wmax - 1); the window starts there (16-byte aligned
+// for cp.async when the tile's rows are), clamped to the tile.
+__device__ __forceinline__ int gx_window_start(const SlabParams& p, int sx, int row_base, bool gx16) {
+  if (p.gx_win <= 0) return row_base;
+  int g0 = max(row_base, lo16(sx) - (p.gx_wmax - 1));
+  if (gx16) g0 &= ~3;
+  return g0;
+}
+
 // Stage gy (slabs js..je), gx (CTA rows) and gz (z window) of candidates
 // meta[0..ns) into consecutive blocks of the staging area, one warp per block.
 // The copies are asynchronous: call cp_async_wait_all() before the barrier.
@@ -884,11 +902,23 @@ __device__ __forceinline__ void stage_tables(const SlabParams& p, const int4* me
     const int64_t a = meta[q].w;
     float* dst = stage + q * p.stage_stride;
     for (int e = lane; e < je - js; e += 32) cp_async4(dst + e, p.ty + a * p.ry + js + e);
-    const float* gx = p.tx + a * p.rx + row_base;
-    if (gx16) {
-      for (int e = lane; e < rows4; e += 32) cp_async16(dst + p.stage_gx + 4 * e, gx + 4 * e);
+    if (p.gx_win > 0) {
+      // window [g0, g0 + gx_win) of the table row around the x-support
+      const int g0 = gx_window_start(p, meta[q].x, row_base, gx16);
+      const float* gx = p.tx + a * p.rx + g0;
+      const int cnt = min(p.gx_win, p.rx - g0);
+      if (gx16) {
+        for (int e = lane; e < (cnt >> 2); e += 32) cp_async16(dst + p.stage_gx + 4 * e, gx + 4 * e);
+      } else {
+        for (int e = lane; e < cnt; e += 32) cp_async4(dst + p.stage_gx + e, gx + e);
+      }
     } else {
-      for (int e = lane; e < rows; e += 32) cp_async4(dst + p.stage_gx + e, gx + e);
+      const float* gx = p.tx + a * p.rx + row_base;
+      if (gx16) {
+        for (int e = lane; e < rows4; e += 32) cp_async16(dst + p.stage_gx + 4 * e, gx + 4 * e);
+      } else {
+        for (int e = lane; e < rows; e += 32) cp_async4(dst + p.stage_gx + e, gx + e);
+      }
     }
     if (SW >= 4) {
       const float* gz = p.tz + a * p.rz + zv0;
@@ -907,7 +937,8 @@ __device__ __forceinline__ void stage_tables(const SlabParams& p, const int4* me
 template <int M>
 __device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* meta, int ns, int ch,
                                                int2* lists, unsigned stage_s, int js, int je,
-                                               int rlo0, int rhi0, int R, Counts<M>& cnt) {
+                                               int rbase, int rlo0, int rhi0, int R,
+                                               Counts<M>& cnt) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int m = 0; m < M; ++m) {
@@ -923,7 +954,9 @@ __device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* 
         if (ch >= 0) hit = hit && __ldg(&p.supp[s.w].w) == ch;
         const int lo = max(lo16(s.y), js) - js, hi = min(hi16(s.y), je) - js;
         const unsigned long long mask = ((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull);
-        ent = make_int2((int)(stage_s + 4u * (unsigned)(q * p.stage_stride)), (int)(unsigned)mask);
+        const int dx = gx_window_start(p, s.x, rbase, (rbase & 3) == 0) - rbase;
+        ent = make_int2((int)((stage_s + 4u * (unsigned)(q * p.stage_stride)) | ((unsigned)dx << 24)),
+                        (int)(unsigned)mask);
       }
       const unsigned bal = __ballot_sync(kFull, hit);
       if (hit) lists[m * p.stage_cap + filled + __popc(bal & ((1u << lane) - 1u))] = ent;
@@ -1003,7 +1036,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
       float* out_b = p.out + T.b * p.C * chan_elems + j0 * p.slab_elems + slot0;
       for (int c = 0; c < p.C; ++c) {
         Counts<M> cnt;
-        build_sublists<M>(p, sh.meta, n, c, lists, stage_s, j0, j1, rlo0, rhi0, R, cnt);
+        build_sublists<M>(p, sh.meta, n, c, lists, stage_s, j0, j1, T.row_base, rlo0, rhi0, R, cnt);
         __syncwarp();
         nz += accumulate_rows<M, SW, true>(out_b + c * chan_elems, p.slab_elems, R * p.D, j1 - j0,
                                            ibase, T.row_end, R, cnt, lists_s, p.stage_cap, gx_off,
@@ -1062,7 +1095,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
           const int4* meta = sh.meta + s0;
           stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
           Counts<M> cnt;
-          build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, rlo0, rhi0, R, cnt);
+          build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, T.row_base, rlo0, rhi0, R, cnt);
           cp_async_wait_all();
           __syncthreads();  // staged tables visible to every warp (lists are warp-private)
 
@@ -1458,7 +1491,7 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
   // Channel fusion (one CTA serves all C channels of its tile from one staged
   // candidate list) for small molecules, whose whole atom list usually fits
   // the staging area; VG_FUSE=0/1 overrides (tuning hook).
-  bool fuse = d.C > 1 && mean_atoms * 2 <= kStageCapMax;
+  bool fuse = d.C > 1 && mean_atoms <= kListCap / 2;
   if (const char* env = getenv("VG_FUSE")) fuse = d.C > 1 && env[0] == '1';
   // Output bytes per CTA (measured on B200): fused CTAs ~1 MiB over all
   // channels; per-channel CTAs 256 KiB, halved for dense molecules (hundreds
@@ -1607,22 +1640,46 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.zw = zw;
   p.rows_per_step = R;
   p.zw_magic = (0x100000000ull / (unsigned long long)zw) + 1ull;
-  // staged block per candidate: gy[pad4(jc)] gx[pad4(M*R)] gz[pad4(zw*width)]
+  // Windowed gx staging (open axes, one shared delta): an atom's x-support
+  // is shorter than 2*t_sat/(delta*s) + 3 edges (fp32 edge arguments differ
+  // from the exact line by < 1e-6 near +-t_sat), so a candidate's gx window
+  // needs support + 2 warp spans + 3 (alignment) rows instead of the tile.
+  p.gx_wmax = 31 / zw + 2;
+  p.gx_win = 0;
+  if (!d.periodic && d.mol_delta == nullptr) {
+    const double span = 2.0001 * (double)VG_TSAT / (d.scale * d.delta[0]);
+    if (span < 4096.0) {
+      const int bound = (int)span + 3;
+      const int win = round_up4(bound + 2 * p.gx_wmax + 1);
+      if (win < round_up4(M * R) && M * R <= 255) p.gx_win = win;
+    }
+  }
+  if (const char* env = getenv("VG_GXWIN")) {
+    if (env[0] == '0') p.gx_win = 0;
+  }
+  // staged block per candidate: gy[pad4(jc)] gx[window or pad4(M*R)] gz[pad4(zw*width)]
   p.stage_gx = (jc + 3) & ~3;
-  p.stage_gz = p.stage_gx + round_up4(M * R);
+  p.stage_gz = p.stage_gx + (p.gx_win > 0 ? p.gx_win : round_up4(M * R));
   p.stage_stride = p.stage_gz + round_up4(zw * width);
-  // staging capacity: what the batch's molecules need (about 2x the mean atom
-  // count), within the byte budget; small molecules keep CTAs small
-  int stage_bytes = kStageBytes, cap_max = kStageCapMax;
-  if (const char* env = getenv("VG_STAGE_KB")) stage_bytes = atoi(env) * 1024;
+  // Level-0 list: only for large molecules scanned without bins (it is used
+  // when a molecule has more than 2*blockDim atoms); with K2 bins the CTA's
+  // bin is its candidate source. Capacity in ints, 16-byte aligned.
+  p.c0_cap = p.bins != nullptr ? 0 : (mean_atoms > 64 ? kC0CapMax : 256);
+  if (const char* env = getenv("VG_C0")) p.c0_cap = atoi(env);
+  // Staging capacity: what the batch's molecules need (about 2x the mean atom
+  // count, at most kListCap), within the shared memory that keeps the
+  // register-limited number of CTAs resident per SM (228 KB per SM, 1 KB
+  // reserved per CTA): the occupancy cliff costs more than extra halving.
+  int cap_max = kListCap;
   if (const char* env = getenv("VG_CAP_MAX")) cap_max = min(atoi(env), kListCap);
-  int cap = stage_bytes / (4 * p.stage_stride);
   const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > cap_max ? cap_max : mean_atoms * 2));
+  const int reg_blocks = max(1, min(8, 65536 / (64 * nt)));   // __launch_bounds__: <= 64 regs
+  const int64_t budget = (int64_t)228 * 1024 / reg_blocks - 1024 - (int64_t)sizeof(SlabShared) -
+                         (int64_t)p.c0_cap * 4 - (int64_t)(M * R + 8 + 3) * 4;
+  const int64_t per_cand = 4 * (int64_t)p.stage_stride + (int64_t)(nt / 32) * M * sizeof(int2);
+  int64_t cap = budget / per_cand;
   if (cap > want) cap = want;
-  p.stage_cap = cap < 1 ? 1 : cap;
-  // level-0 list only pays for large molecules (it is used when a molecule
-  // has more than 2*blockDim atoms); capacity in ints, 16-byte aligned
-  p.c0_cap = mean_atoms > 64 ? kC0CapMax : 256;
+  p.stage_cap = cap < 1 ? 1 : (int)cap;
   // slack: rows >= W of the last step read (and discard) past the last block;
   // then the warp-private sublists (int2 per candidate, row step and warp)
   p.stage_floats = (p.stage_cap * p.stage_stride + M * R + 8 + 3) & ~3;
