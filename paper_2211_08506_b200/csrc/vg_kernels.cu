@@ -243,17 +243,28 @@ constexpr int kWin = 32;   // window edges buffered per lane per pass
 __device__ __forceinline__ bool below_sat(float t) { return t <= -VG_TSAT; }
 __device__ __forceinline__ bool above_sat(float t) { return t >= VG_TSAT; }
 
+// T lanes per row (T = 1, 2, 4, 8; chosen by the launcher so that small
+// batches still fill the GPU): lane `sub` of a row's group evaluates edges
+// pstart + sub + T*i, and the mass g_e = 0.5*(E(e+1) - E(e)) takes E(e+1)
+// from the next lane of the group (from lane 0's next edge for the last
+// lane), so each edge is evaluated once per pass.
+template <int T>
 __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TableParams p) {
-  __shared__ float wbuf[kTableThreads / 32][32][kWin + 1];
+  constexpr int kRowsPerWarp = 32 / T;
+  __shared__ float wbuf[kTableThreads / 32][kRowsPerWarp][kWin + 1];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  const int sub = lane & (T - 1);
+  const int rw = lane / T;
   const int axis = blockIdx.y;
   const int n = p.n[axis];
-  const int64_t atom = (int64_t)blockIdx.x * kTableThreads + threadIdx.x;
+  const int64_t atom0 = (int64_t)blockIdx.x * (kTableThreads / T) + warp * kRowsPerWarp;
+  const int64_t atom = atom0 + rw;
   const bool valid = atom < p.n_atoms;
+  const double s = p.scale;
 
   double rel = 0.0, d = 1.0;
-  int glo = 0, ghi = -1;   // candidate g range (empty for invalid lanes)
+  int glo = 0, ghi = -1;   // candidate g range (empty for invalid rows)
   if (valid) {
     double o = p.origin[axis];
     d = p.delta[axis];
@@ -263,7 +274,6 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
       if (p.mol_delta != nullptr) d = p.mol_delta[b * 3 + axis];
     }
     rel = __dsub_rn(o, p.xyz[atom * 3 + axis]);   // kernels.py:253
-    const double s = p.scale;
     glo = 0;
     ghi = n - 1;
     if (d > 0.0 && isfinite(rel) && isfinite(d)) {
@@ -283,35 +293,42 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
 
   float* tbl_axis = p.tbl[axis];
   const int64_t row = p.row[axis];
-  const int64_t atom0 = atom - lane;
-  int cur = glo;                 // next window edge this lane computes
-  int nz_lo = -1, nz_hi = 0;
-  float e_prev = 0.0f;
-  if (cur <= ghi) e_prev = vg_erf_sat_f32(vg_edge_arg(rel, d, cur, p.scale));
+  int cur = glo;                 // next window edge of this row
+  int nz_lo = INT_MAX, nz_hi = 0;
   bool first = true;
   for (;;) {
-    // pass: up to kWin window values per lane into the warp buffer
+    // pass: up to kWin window values of each row into the warp buffer
     const int pstart = cur;
     const int pend = min(ghi + 1, cur + kWin);
-    for (int e = pstart; e < pend; ++e) {
-      const float e_next = vg_erf_sat_f32(vg_edge_arg(rel, d, e + 1, p.scale));
-      float g = VG_FMUL(0.5f, VG_FSUB(e_next, e_prev));       // kernels.py:260
-      if (p.has_threshold && !(g >= p.threshold)) g = 0.0f;   // kernels.py:271-272
-      if (g != 0.0f) {
-        if (nz_lo < 0) nz_lo = e;
-        nz_hi = e + 1;
+    const int my_it = pend > pstart ? (pend - pstart + T - 1) / T : 0;
+    const int n_it = __reduce_max_sync(kFull, my_it);
+    float e_cur = 0.0f;
+    if (n_it > 0) e_cur = vg_erf_sat_f32(vg_edge_arg(rel, d, pstart + sub, s));
+    for (int i = 0; i < n_it; ++i) {
+      const int e = pstart + sub + T * i;
+      const float e_nxt = vg_erf_sat_f32(vg_edge_arg(rel, d, e + T, s));
+      float up = __shfl_down_sync(kFull, e_cur, 1, T);      // E(e+1) from lane sub+1
+      const float wrap = __shfl_sync(kFull, e_nxt, 0, T);   // E(pstart + T*(i+1))
+      if (sub == T - 1) up = wrap;
+      if (e < pend) {
+        float g = VG_FMUL(0.5f, VG_FSUB(up, e_cur));            // kernels.py:260
+        if (p.has_threshold && !(g >= p.threshold)) g = 0.0f;   // kernels.py:271-272
+        if (g != 0.0f) {
+          nz_lo = min(nz_lo, e);
+          nz_hi = max(nz_hi, e + 1);
+        }
+        wbuf[warp][rw][e - pstart] = g;
       }
-      wbuf[warp][lane][e - pstart] = g;
-      e_prev = e_next;
+      e_cur = e_nxt;
     }
     cur = max(pend, cur);
     __syncwarp();
     // coalesced write-out, one row at a time
-    for (int r = 0; r < 32; ++r) {
-      const int r_lo = __shfl_sync(kFull, glo, r);
-      const int r_hi = __shfl_sync(kFull, ghi, r);
-      const int r_ps = __shfl_sync(kFull, pstart, r);
-      const int r_pe = __shfl_sync(kFull, pend, r);
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int r_lo = __shfl_sync(kFull, glo, r * T);
+      const int r_hi = __shfl_sync(kFull, ghi, r * T);
+      const int r_ps = __shfl_sync(kFull, pstart, r * T);
+      const int r_pe = __shfl_sync(kFull, pend, r * T);
       if (atom0 + r >= p.n_atoms) break;
       if (!first && r_pe <= r_ps) continue;
       float* dst = tbl_axis + (atom0 + r) * row;
@@ -326,9 +343,16 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
     if (!__any_sync(kFull, cur <= ghi)) break;
     __syncwarp();
   }
-  if (valid) {
-    const int slo = nz_lo < 0 ? 0 : nz_lo;   // _support_of: (0, 0) when all zero
-    const int shi = nz_lo < 0 ? 0 : nz_hi;
+  // support of the row: first / last nonzero over the group's lanes
+#pragma unroll
+  for (int o = 1; o < T; o <<= 1) {
+    nz_lo = min(nz_lo, __shfl_xor_sync(kFull, nz_lo, o, T));
+    nz_hi = max(nz_hi, __shfl_xor_sync(kFull, nz_hi, o, T));
+  }
+  if (valid && sub == 0) {
+    const bool any = nz_lo != INT_MAX;
+    const int slo = any ? nz_lo : 0;   // _support_of: (0, 0) when all zero
+    const int shi = any ? nz_hi : 0;
     p.supp[atom * 4 + axis] = slo | (shi << 16);
     if (axis == 0) p.supp[atom * 4 + 3] = p.channel[atom];
   }
@@ -1327,8 +1351,20 @@ int launch_tables(const vg_batch_desc* d, const vg_ws_layout& L, char* ws, cudaS
   p.threshold = d->threshold;
   p.periodic = d->periodic != 0;
   if (!p.periodic) {
-    const int64_t blocks = (d->n_atoms + kTableThreads - 1) / kTableThreads;
-    vg_tables_open_kernel<<<dim3((unsigned)blocks, 3), kTableThreads, 0, st>>>(p);
+    // lanes per row: more lanes only for small batches (K1 otherwise runs
+    // beside the previous batch's K3 in GridPipeline, where wider K1 CTAs
+    // take more of K3's SM slots; measured on B200)
+    int T = 1;
+    while (T < 8 && d->n_atoms * 3 * T < 148 * 384) T *= 2;
+    if (const char* env = getenv("VG_K1T")) T = atoi(env);
+    const int64_t rows_per_block = kTableThreads / T;
+    const dim3 grid((unsigned)((d->n_atoms + rows_per_block - 1) / rows_per_block), 3);
+    switch (T) {
+      case 2: vg_tables_open_kernel<2><<<grid, kTableThreads, 0, st>>>(p); break;
+      case 4: vg_tables_open_kernel<4><<<grid, kTableThreads, 0, st>>>(p); break;
+      case 8: vg_tables_open_kernel<8><<<grid, kTableThreads, 0, st>>>(p); break;
+      default: vg_tables_open_kernel<1><<<grid, kTableThreads, 0, st>>>(p); break;
+    }
     return check_launch("vg_tables_open_kernel");
   }
   const int64_t warps = d->n_atoms * 3;
