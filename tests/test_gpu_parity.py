@@ -83,7 +83,10 @@ def test_axis_tables_match_golden(case):
     (0.7, (31, 65, 129), 20.0, 1e-4),    # threshold
     (0.7, (31, 65, 129), 20.0, -1.0),    # negative threshold keeps zeros
 ])
-def test_axis_tables_window_search_vs_oracle(sigma, shape, extent, thr):
+@pytest.mark.parametrize("lanes", [None, "2", "4", "8"])
+def test_axis_tables_window_search_vs_oracle(sigma, shape, extent, thr, lanes, monkeypatch):
+    if lanes is not None:
+        monkeypatch.setenv("VG_K1T", lanes)   # K1 lanes per row (default: by batch size)
     rng = np.random.default_rng(int(sigma * 1000) + shape[0])
     n_mol, per = 7, 111
     n = n_mol * per
