@@ -83,8 +83,8 @@ constexpr int row_minb(int m) { return m == 1 ? VG_ROW_MINB1 : VG_ROW_MINB; }
 constexpr int64_t kTaskBytes = 262144;       // K3: output bytes per CTA (y-chunk sizing)
 constexpr int64_t kFusedTaskBytes = 1048576; // ... per channel-fused CTA, all channels
 constexpr int64_t kMinCtas = 148 * 8;         // K3: CTAs a launch should at least offer
-constexpr int kMaxBins = 2048;                // K2: bins (channels x y-chunks) per molecule
-constexpr int kBinWarps = 8;                  // K2: warps per molecule CTA
+constexpr int kMaxBins = 1024;                // K2: bins (channels x y-chunks) per molecule
+constexpr int kBinWarps = 32;                 // K2: warps per molecule CTA
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
