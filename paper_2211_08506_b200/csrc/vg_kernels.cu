@@ -90,6 +90,18 @@ constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 int round_up4(int v) { return (v + 3) & ~3; }
 
+// Tuning / test hooks (VG_* environment variables, read at launch time so
+// that tests can switch code paths inside one process): the integer value of
+// `name` if it is set, parses fully and lies in [lo, hi]; otherwise dflt.
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = getenv(name);
+  if (v == nullptr || *v == '\0') return dflt;
+  char* end = nullptr;
+  const long x = strtol(v, &end, 10);
+  if (*end != '\0' || x < lo || x > hi) return dflt;
+  return (int)x;
+}
+
 // ---------------------------------------------------------------------------
 // K1: per-atom axis tables
 // ---------------------------------------------------------------------------
@@ -1356,7 +1368,8 @@ int launch_tables(const vg_batch_desc* d, const vg_ws_layout& L, char* ws, cudaS
     // take more of K3's SM slots; measured on B200)
     int T = 1;
     while (T < 8 && d->n_atoms * 3 * T < 148 * 384) T *= 2;
-    if (const char* env = getenv("VG_K1T")) T = atoi(env);
+    T = env_int("VG_K1T", T, 1, 8);
+    if (T & (T - 1)) T = 1;
     const int64_t rows_per_block = kTableThreads / T;
     const dim3 grid((unsigned)((d->n_atoms + rows_per_block - 1) / rows_per_block), 3);
     switch (T) {
@@ -1415,9 +1428,9 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   const int base = spr / gcd_int(32, spr) * 32;  // lcm(32, spr)
   if (base > kRowThreads) return false;
   double best = 1e30;
-  const char* fq = getenv("VG_PLAN_Q");   // tuning hook: force the thread multiple
+  int fq = env_int("VG_PLAN_Q", 0, 1, kRowThreads / base);   // hook: force the thread multiple
   for (int q = 1; base * q <= kRowThreads; ++q) {
-    if (fq != nullptr && atoi(fq) != q) continue;
+    if (fq != 0 && fq != q) continue;
     const int t = base * q, r = t / spr;
     const int need = (W + r - 1) / r;
     int m = need < 8 ? need : 8;
@@ -1470,11 +1483,8 @@ void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const S
 // slots, 8-slot (32-float, 128 B) windows for wider rows so warps cull in z
 // too. VG_ZW overrides (tuning hook).
 int pick_zw(int spr, int sw) {
-  const char* env = getenv("VG_ZW");
-  if (env != nullptr) {
-    const int v = atoi(env);
-    if (v > 0 && spr % v == 0) return v;
-  }
+  const int v = env_int("VG_ZW", 0, 1, spr);
+  if (v > 0 && spr % v == 0) return v;
   const int win = 32 / sw;  // 32-float (128 B) windows on rows wider than 64 floats
   if (spr * sw > 64 && win > 0 && spr % win == 0) return win;
   return spr;
@@ -1484,12 +1494,9 @@ int pick_zw(int spr, int sw) {
 // apart) when D % 8 == 0, else 4 (float4), else 1. VG_SW overrides.
 int pick_sw(int D, bool aligned16) {
   int sw = !aligned16 || D % 4 != 0 ? 1 : (D % 8 == 0 ? 8 : 4);
-  const char* env = getenv("VG_SW");
-  if (env != nullptr) {
-    const int v = atoi(env);
-    if ((v == 1) || (v == 4 && aligned16 && D % 4 == 0) || (v == 8 && aligned16 && D % 8 == 0))
-      sw = v;
-  }
+  const int v = env_int("VG_SW", 0, 1, 8);
+  if ((v == 1) || (v == 4 && aligned16 && D % 4 == 0) || (v == 8 && aligned16 && D % 8 == 0))
+    sw = v;
   return sw;
 }
 
@@ -1510,9 +1517,9 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
   memset(P, 0, sizeof *P);
   P->sw = pick_sw(d.D, aligned16);
   const int64_t slab = (int64_t)d.W * d.D;
-  const char* force = getenv("VG_FORCE_GENERIC");
+  const bool force = env_int("VG_FORCE_GENERIC", 0, 0, 1) == 1;
   P->zw = pick_zw(d.D / P->sw, P->sw);
-  P->rows_ok = !(force && force[0] == '1') &&
+  P->rows_ok = !force &&
                plan_rows(P->zw, d.W, &P->nt, &P->R, &P->M, &P->row_blocks);
   // the generic kernel works in float4 or float slots
   P->vec = P->rows_ok ? P->sw >= 4 : (d.D % 4 == 0 && aligned16);
@@ -1528,7 +1535,7 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
   // candidate list) for small molecules, whose whole atom list usually fits
   // the staging area; VG_FUSE=0/1 overrides (tuning hook).
   bool fuse = d.C > 1 && mean_atoms <= kListCap / 2;
-  if (const char* env = getenv("VG_FUSE")) fuse = d.C > 1 && env[0] == '1';
+  fuse = d.C > 1 && env_int("VG_FUSE", fuse ? 1 : 0, 0, 1) == 1;
   // Output bytes per CTA (measured on B200): fused CTAs ~1 MiB over all
   // channels; per-channel CTAs 256 KiB, halved for dense molecules (hundreds
   // of candidates per tile), whose shorter y-chunks halve less often.
@@ -1536,7 +1543,8 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
   // small batches: keep at least ~8 CTAs per SM in flight
   const int64_t total_bytes = d.n_molecules * (int64_t)d.C * d.H * slab * 4;
   if (task_bytes > total_bytes / kMinCtas) task_bytes = total_bytes / kMinCtas;
-  if (const char* env = getenv("VG_TASK_KB")) task_bytes = (int64_t)atoi(env) * 1024;
+  const int task_kb = env_int("VG_TASK_KB", 0, 1, 1 << 20);
+  if (task_kb > 0) task_bytes = (int64_t)task_kb * 1024;
   if (fuse) task_bytes = (task_bytes + d.C - 1) / d.C;   // per channel
   // y-slabs per CTA: aim for task_bytes of output (<= 32 for the slab masks),
   // then even out the chunks
@@ -1556,9 +1564,7 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
 // otherwise scan thousands of atoms: per-channel CTAs, > 2*256 atoms on
 // average, and a bounded number of bins per molecule.
 bool want_bins(const vg_batch_desc& d, const SlabPlan& P) {
-  if (const char* env = getenv("VG_BINS")) {
-    if (env[0] == '0') return false;
-  }
+  if (env_int("VG_BINS", 1, 0, 1) == 0) return false;
   if (!P.rows_ok || P.fuse || d.periodic) return false;
   if (P.mean_atoms <= 2 * kRowThreads) return false;
   const int64_t nb = (int64_t)d.C * P.n_jchunks;
@@ -1690,9 +1696,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
       if (win < round_up4(M * R) && M * R <= 255) p.gx_win = win;
     }
   }
-  if (const char* env = getenv("VG_GXWIN")) {
-    if (env[0] == '0') p.gx_win = 0;
-  }
+  if (env_int("VG_GXWIN", 1, 0, 1) == 0) p.gx_win = 0;
   // staged block per candidate: gy[pad4(jc)] gx[window or pad4(M*R)] gz[pad4(zw*width)]
   p.stage_gx = (jc + 3) & ~3;
   p.stage_gz = p.stage_gx + (p.gx_win > 0 ? p.gx_win : round_up4(M * R));
@@ -1701,13 +1705,13 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   // when a molecule has more than 2*blockDim atoms); with K2 bins the CTA's
   // bin is its candidate source. Capacity in ints, 16-byte aligned.
   p.c0_cap = p.bins != nullptr ? 0 : (mean_atoms > 64 ? kC0CapMax : 256);
-  if (const char* env = getenv("VG_C0")) p.c0_cap = atoi(env);
+  p.c0_cap = env_int("VG_C0", p.c0_cap, 0, kC0CapMax);
   // Staging capacity: what the batch's molecules need (about 2x the mean atom
   // count, at most kListCap), within the shared memory that keeps the
   // register-limited number of CTAs resident per SM (228 KB per SM, 1 KB
   // reserved per CTA): the occupancy cliff costs more than extra halving.
   int cap_max = kListCap;
-  if (const char* env = getenv("VG_CAP_MAX")) cap_max = min(atoi(env), kListCap);
+  cap_max = env_int("VG_CAP_MAX", cap_max, 1, kListCap);
   const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > cap_max ? cap_max : mean_atoms * 2));
   const int reg_blocks = max(1, min(8, 65536 / (64 * nt)));   // __launch_bounds__: <= 64 regs
   const int64_t budget = (int64_t)228 * 1024 / reg_blocks - 1024 - (int64_t)sizeof(SlabShared) -
