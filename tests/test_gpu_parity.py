@@ -395,6 +395,30 @@ def test_candidate_bins_vs_oracle_and_unbinned(policy, monkeypatch):
         assert st.voxel_writes == rs["voxel_writes"] and st.nonzero_voxels == rs["nonzero_voxels"]
 
 
+@pytest.mark.parametrize("env", [{}, {"VG_FUSE": "0"}, {"VG_GXWIN": "0"}, {"VG_FUSE": "1", "VG_SW": "4"}])
+def test_many_channels_threshold_paths_vs_oracle(env, monkeypatch):
+    """Small molecules over 12 channels with a threshold: the channel-fused
+    path (default), per-channel CTAs, full-tile gx staging and float4 slots
+    all match the oracle bit for bit."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(123)
+    sizes = rng.integers(1, 40, size=23)
+    sizes[5] = 0
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(offsets[-1])
+    xyz = rng.uniform(-1.0, 9.0, (n, 3))
+    ch = rng.integers(0, 12, n).astype(np.int32)
+    shape = (36, 28, 40)
+    spec = vg.GridSpec(shape, 12, vg.BoundingBox((0, 0, 0), (8.0, 8.0, 8.0)), 0.4)
+    grids, st = vg.generate_packed(offsets, ch, xyz, spec, threshold=1e-3)
+    ref, rs = orc.batch(offsets, ch, xyz, orc.Geometry(shape, 12, (0, 0, 0), (8.0, 8.0, 8.0), 0.4),
+                        threshold=1e-3, workers=orc.host_cores())
+    assert_bitwise(grids.cpu().numpy(), ref, f"many channels {env}")
+    assert [int(v) for v in st[:, 0].cpu()] == [r["voxel_writes"] for r in rs]
+    assert [int(v) for v in st[:, 1].cpu()] == [r["nonzero_voxels"] for r in rs]
+
+
 @pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 7), (5, 3, 4), (33, 31, 36), (4, 70, 8)])
 def test_odd_shapes_vs_oracle(shape):
     rng = np.random.default_rng(sum(shape))
