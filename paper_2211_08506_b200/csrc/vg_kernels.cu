@@ -580,9 +580,9 @@ __device__ __forceinline__ void add_terms(float& acc, float pyx, const float* gz
 }
 
 __device__ __forceinline__ void store_slot(float* slab, int f, const float4& v) {
-  reinterpret_cast<float4*>(slab)[f] = v;
+  __stcs(reinterpret_cast<float4*>(slab) + f, v);
 }
-__device__ __forceinline__ void store_slot(float* slab, int f, const float& v) { slab[f] = v; }
+__device__ __forceinline__ void store_slot(float* slab, int f, const float& v) { __stcs(slab + f, v); }
 
 __device__ long long block_sum(SlabShared& sh, long long v) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
@@ -773,6 +773,19 @@ struct Counts {
 
 // Slot I/O. SW=8 slots are two float4 half a z-window apart ("half" floats),
 // so that every 128-bit warp store still covers 512 contiguous bytes.
+// Output stores are streaming (st.global.cs: evict-first in L2). The grids
+// are never re-read by the kernel, and streaming them through L2 normally
+// would evict the K1 tables that later CTAs stage from.
+#ifndef VG_EXP_PLAINST
+__device__ __forceinline__ void st_slot(float* p, const float& v, int) { __stcs(p, v); }
+__device__ __forceinline__ void st_slot(float* p, const float4& v, int) {
+  __stcs(reinterpret_cast<float4*>(p), v);
+}
+__device__ __forceinline__ void st_slot(float* p, const Slot8& v, int half) {
+  __stcs(reinterpret_cast<float4*>(p), v.a);
+  __stcs(reinterpret_cast<float4*>(p + half), v.b);
+}
+#else
 __device__ __forceinline__ void st_slot(float* p, const float& v, int) { *p = v; }
 __device__ __forceinline__ void st_slot(float* p, const float4& v, int) {
   *reinterpret_cast<float4*>(p) = v;
@@ -781,6 +794,7 @@ __device__ __forceinline__ void st_slot(float* p, const Slot8& v, int half) {
   *reinterpret_cast<float4*>(p) = v.a;
   *reinterpret_cast<float4*>(p + half) = v.b;
 }
+#endif
 __device__ __forceinline__ void ld_slot(float& v, const float* p, int) { v = *p; }
 __device__ __forceinline__ void ld_slot(float4& v, const float* p, int) {
   v = *reinterpret_cast<const float4*>(p);
@@ -815,6 +829,9 @@ __device__ __forceinline__ void term_of(unsigned ent, unsigned gy_off, unsigned 
 template <typename Slot>
 __device__ __forceinline__ void walk_group(unsigned act, int ent_x, unsigned gy_off, unsigned gxm,
                                            unsigned gz_off, unsigned halfb, Slot& acc) {
+#ifdef VG_EXP_NOWALK
+  return;   // experiment build only: measures the kernel without the hot loop
+#endif
   while (act != 0u) {
     const int b0 = __ffs(act) - 1;
     act &= act - 1u;
@@ -931,6 +948,9 @@ template <int SW>
 __device__ __forceinline__ void stage_tables(const SlabParams& p, const int4* meta, int ns,
                                              float* stage, int js, int je, int row_base, int rows,
                                              int zv0, int zv1) {
+#ifdef VG_EXP_NOSTAGE
+  return;   // experiment build only
+#endif
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool gx16 = (row_base & 3) == 0;   // table rows are 16-byte aligned (pad4)
   const int rows4 = (rows + 3) >> 2;
@@ -1261,10 +1281,12 @@ __global__ void vg_erf_kernel(const float* __restrict__ t, float* __restrict__ o
     out[i] = vg_erf_f32(t[i]);
 }
 
+// Write-ceiling probe: grid-stride streaming 128-bit stores (as K3 stores).
+// (A contiguous chunk per CTA measured slower: 5.5 vs 6.5 TB/s.)
 __global__ void vg_fill_kernel(float4* __restrict__ out, int64_t n4, float4 v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = v;
+    __stcs(out + i, v);
 }
 
 __global__ void vg_fill_tail_kernel(float* __restrict__ out, int64_t n, float v) {
