@@ -404,7 +404,9 @@ struct SlabParams {
   int stage_gz;         // offset of gz inside a staged block
   int stage_floats;     // floats of the staging area (sublists follow it)
   int c0_cap;           // level-0 candidate capacity (ints before the staging area)
-  int fuse_channels;    // 1: one CTA serves every channel (grid.y == 1)
+  int fuse_channels;    // 1: one CTA serves every channel
+  int tasks;            // tiles per (molecule, channel): y-chunks x row-blocks x z-blocks
+  int n_molecules;
   int gx_win;           // staged gx rows per candidate (window), 0: all CTA rows
   int gx_wmax;          // rows one warp spans in a row step (window padding)
   // K2 candidate bins (NULL: scan the molecule's atoms)
@@ -1033,9 +1035,28 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   const int tid = threadIdx.x, warp = tid >> 5;
 
   RowTile T;
-  T.b = blockIdx.x;
-  T.c = blockIdx.y;
-  int t = blockIdx.z, zblk = 0, rblk = 0;
+  // Linear CTA index. Channel-fused CTAs: the tiles of one molecule are
+  // adjacent, so the CTAs staging the same atoms' tables run close together
+  // while those are in L2. Per-channel CTAs (large molecules): molecule
+  // fastest, which spreads the dense central tiles of a cluster over the
+  // launch (measured better for cfg3).
+  int t, zblk = 0, rblk = 0;
+  {
+    const unsigned lin = blockIdx.x;
+    if (p.fuse_channels) {
+      const unsigned b = lin / (unsigned)p.tasks;
+      t = (int)(lin - b * (unsigned)p.tasks);
+      T.b = b;
+      T.c = 0;
+    } else {
+      const unsigned nb = (unsigned)p.n_molecules;
+      const unsigned rest = lin / nb;
+      T.b = lin - rest * nb;
+      const unsigned tt = rest / (unsigned)p.C;
+      T.c = (int)(rest - tt * (unsigned)p.C);
+      t = (int)tt;
+    }
+  }
   if (p.z_blocks > 1) {
     zblk = t % p.z_blocks;
     t /= p.z_blocks;
@@ -1670,8 +1691,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int jc = P.jc;
   p.jc = jc;
   p.n_jchunks = P.n_jchunks;
-  if (d.C > 65535 || (int64_t)p.n_jchunks * row_blocks * z_blocks > 65535 ||
-      d.n_molecules > INT_MAX)
+  if ((int64_t)p.n_jchunks * row_blocks * z_blocks > INT_MAX / 2)
     return set_error(VG_ERR_INVALID, "grid too large for the slab kernel");
   // K2: ordered per-(molecule, channel, y-chunk) candidate bins, when the
   // workspace was laid out for this plan's chunks
@@ -1748,8 +1768,11 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const size_t smem = (size_t)p.c0_cap * sizeof(int) + (size_t)p.stage_floats * sizeof(float) +
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
   p.fuse_channels = fuse ? 1 : 0;
-  const dim3 grid((unsigned)d.n_molecules, fuse ? 1u : (unsigned)d.C,
-                  (unsigned)(p.n_jchunks * row_blocks * z_blocks));
+  p.tasks = p.n_jchunks * row_blocks * z_blocks;
+  p.n_molecules = (int)d.n_molecules;
+  const int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
+  if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
+  const dim3 grid((unsigned)ctas);
   if (sw == 8)
     launch_rows<8>(M, grid, nt, smem, st, p);
   else if (sw == 4)
