@@ -335,6 +335,33 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
     }
     cur = max(pend, cur);
     __syncwarp();
+    if (first && !__any_sync(kFull, cur <= ghi)) {
+      // Every row's window fit this pass (the common case): whole rows,
+      // zeros and window, padding included, as float4 stores; Lp lanes
+      // (a power of two >= the row's float4 count, <= 32) per row.
+      const int n4 = (n + 3) >> 2;
+      int lp = 1;
+      while (lp < n4 && lp < 32) lp <<= 1;
+      const int rows_per_it = 32 / lp;
+      const int sub4 = lane & (lp - 1), rsel = lane / lp;
+      for (int r0 = 0; r0 < kRowsPerWarp; r0 += rows_per_it) {
+        const int r = r0 + rsel;
+        const int src = min(r, kRowsPerWarp - 1) * T;
+        const int r_ps = __shfl_sync(kFull, pstart, src);
+        const int r_pe = __shfl_sync(kFull, pend, src);
+        if (r >= kRowsPerWarp || atom0 + r >= p.n_atoms) continue;
+        float4* dst4 = reinterpret_cast<float4*>(tbl_axis + (atom0 + r) * row);
+        for (int c4 = sub4; c4 < n4; c4 += lp) {
+          const int e = 4 * c4;
+          float v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            v[i] = (e + i >= r_ps && e + i < r_pe) ? wbuf[warp][r][e + i - r_ps] : 0.0f;
+          dst4[c4] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      }
+      break;
+    }
     // coalesced write-out, one row at a time
     for (int r = 0; r < kRowsPerWarp; ++r) {
       const int r_lo = __shfl_sync(kFull, glo, r * T);

@@ -1,5 +1,5 @@
 """Per-CUDA-source-line instructions and stall samples of an ncu report:
-python scripts/ncu_lines.py rep [top]  (needs -lineinfo builds)."""
+python scripts/ncu_lines.py rep [top] [kernel regex]  (needs -lineinfo builds)."""
 import csv
 import io
 import subprocess
@@ -7,8 +7,9 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
-                     capture_output=True, text=True).stdout
+kfilter = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv",
+                      "--print-source=cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(r for r in rows if r and r[0] == "Line No")
 ie = hdr.index("Instructions Executed")
