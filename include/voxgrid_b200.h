@@ -124,6 +124,9 @@ int vg_fill_f32(float* out, int64_t n, float value, void* stream);
  * np.exp on float32 (numpy SIMD algorithm) and the Bürmann erf. */
 int vg_exp_f32_host(const float* x, float* out, size_t n);
 int vg_erf_f32_host(const float* t, float* out, size_t n);
+/* The saturated erf K1 evaluates: +-1 beyond +-VG_TSAT, else the series with
+ * the exp range checks dropped (bit-identical to vg_erf_f32_host). */
+int vg_erf_sat_f32_host(const float* t, float* out, size_t n);
 
 /* Thread-local description of the last error (empty string if none). */
 const char* vg_last_error(void);

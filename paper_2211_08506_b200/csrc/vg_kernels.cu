@@ -116,6 +116,8 @@ struct TableParams {
   double origin[3];
   double delta[3];
   double scale;
+  double tsat_over_s;   // t_sat / scale (window estimates)
+  double inv_delta[3];  // 1 / delta (window estimates)
   int64_t n_atoms;
   int64_t n_molecules;
   int n[3];
@@ -290,8 +292,10 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
     ghi = n - 1;
     if (d > 0.0 && isfinite(rel) && isfinite(d)) {
       // estimates, then exact correction against the fp32 edge arguments
-      const double ea = (-(double)VG_TSAT / s - rel) / d;
-      const double eb = ((double)VG_TSAT / s - rel) / d;
+      // (estimates only: multiply by a reciprocal computed once)
+      const double inv_d = p.mol_delta != nullptr ? 1.0 / d : p.inv_delta[axis];
+      const double ea = (-p.tsat_over_s - rel) * inv_d;
+      const double eb = (p.tsat_over_s - rel) * inv_d;
       int a = ea <= 0.0 ? 0 : (ea >= (double)(n + 1) ? n + 1 : (int)ceil(ea));
       int b = eb < 0.0 ? -1 : (eb >= (double)n ? n : (int)floor(eb));
       while (a > 0 && !below_sat(vg_edge_arg(rel, d, a - 1, s))) --a;
@@ -1421,6 +1425,8 @@ int launch_tables(const vg_batch_desc* d, const vg_ws_layout& L, char* ws, cudaS
     p.delta[a] = d->delta[a];
   }
   p.scale = d->scale;
+  p.tsat_over_s = (double)VG_TSAT / d->scale;
+  for (int a = 0; a < 3; ++a) p.inv_delta[a] = 1.0 / d->delta[a];
   p.n_atoms = d->n_atoms;
   p.n_molecules = d->n_molecules;
   p.n[0] = d->W;
@@ -1878,6 +1884,12 @@ VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
 VG_API int vg_exp_f32_host(const float* x, float* out, size_t n) {
   if (n > 0 && (x == nullptr || out == nullptr)) return set_error(VG_ERR_INVALID, "NULL pointer");
   for (size_t i = 0; i < n; ++i) out[i] = vg_exp_f32(x[i]);
+  return VG_OK;
+}
+
+VG_API int vg_erf_sat_f32_host(const float* t, float* out, size_t n) {
+  if (n > 0 && (t == nullptr || out == nullptr)) return set_error(VG_ERR_INVALID, "NULL pointer");
+  for (size_t i = 0; i < n; ++i) out[i] = vg_erf_sat_f32(t[i]);
   return VG_OK;
 }
 

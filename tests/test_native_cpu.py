@@ -122,3 +122,21 @@ def test_erf_saturation_threshold(lib):
         assert np.all(_host(lib.vg_erf_f32_host, t) == 1.0)
         assert np.all(_host(lib.vg_erf_f32_host, -t) == -1.0)
     assert _host(lib.vg_erf_f32_host, np.array([below], np.float32))[0] < 1.0
+
+
+def test_saturated_erf_equals_full_erf(lib):
+    """K1's vg_erf_sat_f32 (range checks of exp dropped inside |t| < t_sat)
+    is bit-identical to vg_erf_f32 on a strided sample of every float in
+    (-t_sat, t_sat), the neighbourhood of +-t_sat, zeros, infinities and NaN.
+    (The full 2^31-float sweep was run once when it was introduced.)"""
+    tsat = np.float32(float.fromhex("0x1.01a2a2p+2"))
+    hi = int(tsat.view(np.uint32))
+    pos = np.arange(0, hi + 4096, 61, dtype=np.uint32).view(np.float32)
+    near = np.arange(hi - 4096, hi + 4096, dtype=np.uint32).view(np.float32)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, 1e-45, 3.0, 4.0255513], np.float32)
+    for t in (pos, -pos, near, -near, special):
+        a = _host(lib.vg_erf_sat_f32_host, t)
+        b = _host(lib.vg_erf_f32_host, t)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    nan = _host(lib.vg_erf_sat_f32_host, np.array([np.nan], np.float32))
+    assert np.isnan(nan[0])
