@@ -1555,6 +1555,34 @@ void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const S
   }
 }
 
+// Registers per thread of the row kernel instance (queried once): the
+// shared-memory budget keeps as many CTAs resident as the registers allow.
+template <int SW>
+int rows_regs_sw(int M) {
+  static int regs[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int m = M < 1 ? 1 : (M > 8 ? 8 : M);
+  if (regs[m] == 0) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (m) {
+      case 1: e = cudaFuncGetAttributes(&a, vg_slab_kernel<1, SW>); break;
+      case 2: e = cudaFuncGetAttributes(&a, vg_slab_kernel<2, SW>); break;
+      case 3: e = cudaFuncGetAttributes(&a, vg_slab_kernel<3, SW>); break;
+      case 4: e = cudaFuncGetAttributes(&a, vg_slab_kernel<4, SW>); break;
+      case 5: e = cudaFuncGetAttributes(&a, vg_slab_kernel<5, SW>); break;
+      case 6: e = cudaFuncGetAttributes(&a, vg_slab_kernel<6, SW>); break;
+      case 7: e = cudaFuncGetAttributes(&a, vg_slab_kernel<7, SW>); break;
+      default: e = cudaFuncGetAttributes(&a, vg_slab_kernel<8, SW>); break;
+    }
+    regs[m] = e == cudaSuccess && a.numRegs > 0 ? a.numRegs : 64;
+  }
+  return regs[m];
+}
+
+int rows_regs(int sw, int M) {
+  return sw == 8 ? rows_regs_sw<8>(M) : (sw == 4 ? rows_regs_sw<4>(M) : rows_regs_sw<1>(M));
+}
+
 // z window (slots per row segment) of the row kernel: whole rows up to 16
 // slots, 8-slot (32-float, 128 B) windows for wider rows so warps cull in z
 // too. VG_ZW overrides (tuning hook).
@@ -1788,7 +1816,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   int cap_max = kListCap;
   cap_max = env_int("VG_CAP_MAX", cap_max, 1, kListCap);
   const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > cap_max ? cap_max : mean_atoms * 2));
-  const int reg_blocks = max(1, min(8, 65536 / (64 * nt)));   // __launch_bounds__: <= 64 regs
+  const int regs = (rows_regs(sw, M) + 7) & ~7;   // allocation granularity
+  const int reg_blocks = max(1, min(2048 / nt, 65536 / (regs * nt)));
   const int64_t budget = (int64_t)228 * 1024 / reg_blocks - 1024 - (int64_t)sizeof(SlabShared) -
                          (int64_t)p.c0_cap * 4 - (int64_t)(M * R + 8 + 3) * 4;
   const int64_t per_cand = 4 * (int64_t)p.stage_stride + (int64_t)(nt / 32) * M * sizeof(int2);
