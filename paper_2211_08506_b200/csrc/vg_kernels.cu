@@ -1334,7 +1334,8 @@ __global__ void vg_erf_kernel(const float* __restrict__ t, float* __restrict__ o
 }
 
 // Write-ceiling probe: grid-stride streaming 128-bit stores (as K3 stores).
-// (A contiguous chunk per CTA measured slower: 5.5 vs 6.5 TB/s.)
+// (scripts/probes/write_ceiling.cu: this pattern with 148*64 CTAs is the
+// fastest of the simple write patterns on B200, ~6.87 TB/s.)
 __global__ void vg_fill_kernel(float4* __restrict__ out, int64_t n4, float4 v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1901,7 +1902,7 @@ VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
   const int64_t n4 = n / 4;
   if (n4 > 0) {
     int64_t blocks = (n4 + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 64) blocks = 148 * 64;
     vg_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(out), n4,
                                                       make_float4(value, value, value, value));
   }
