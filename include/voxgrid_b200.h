@@ -25,7 +25,7 @@ extern "C" {
 #define VG_ERR_CUDA -2      /* a CUDA launch or runtime call failed             */
 #define VG_ERR_WORKSPACE -3 /* workspace pointer NULL or too small              */
 
-#define VG_ABI_VERSION 2
+#define VG_ABI_VERSION 3
 
 /* One batch of molecules in CSR form plus the grid geometry.
  *
@@ -92,6 +92,37 @@ int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspace,
  * regenerate grids from cached tables. */
 int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
                  size_t workspace_bytes, vg_mol_stats* stats, void* stream);
+
+/* One pipelined submission (the loader stage around the path: GridPipeline,
+ * paper_2211_08506_b200/loader.py; it replaces the per-batch body of
+ * GaussianVoxelizer.transform, estimator.py:134-151, minus the np.stack):
+ * copy_stream  waits ev_wait, H2D of the host CSR arrays (when h_* != NULL)
+ *              into desc->offsets/channel/xyz, records ev_copied;
+ * tables_stream waits ev_wait + ev_copied, K1, records ev_tabled;
+ * compute_stream waits ev_wait + ev_tabled, K2/K3, then the D2H of the
+ *              per-grid stats into h_stats (when != NULL), records ev_done.
+ * Events are caller-created cudaEvent_t (passed as void*); ev_wait may be
+ * NULL and may be the same event as ev_done (the wait uses its previous
+ * record). Returns at once: no host synchronisation. Host buffers must stay
+ * valid (pinned for asynchronous copies) until ev_copied / ev_done.
+ * VG_ERR_WORKSPACE sets *ws_needed (if non-NULL) to the bytes required. */
+typedef struct vg_submit_args {
+  const void* h_offsets;   /* host [B+1] int64, or NULL: desc->offsets already filled   */
+  const void* h_channel;   /* host [n_atoms] int32, or NULL                              */
+  const void* h_xyz;       /* host [n_atoms*3] fp64, or NULL                             */
+  void* h_stats;           /* host [B] vg_mol_stats (pinned), or NULL: no read-back      */
+  void* copy_stream;
+  void* tables_stream;
+  void* compute_stream;
+  void* ev_wait;
+  void* ev_copied;
+  void* ev_tabled;
+  void* ev_done;
+  size_t* ws_needed;
+} vg_submit_args;
+
+int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* args, float* out,
+                  void* workspace, size_t workspace_bytes, vg_mol_stats* stats);
 
 /* Replaces fused_axis_tables (kernels.py:217-274) for every atom of the
  * batch: fills the workspace tables + supports (layout above). Test hook and

@@ -29,6 +29,7 @@ NVCC_FLAGS = [
 ]
 
 VG_OK = 0
+VG_ERR_WORKSPACE = -3
 
 
 class NativeUnavailable(ImportError):
@@ -73,6 +74,23 @@ class VgWsLayout(ctypes.Structure):
     ]
 
 
+class VgSubmitArgs(ctypes.Structure):
+    _fields_ = [
+        ("h_offsets", ctypes.c_void_p),
+        ("h_channel", ctypes.c_void_p),
+        ("h_xyz", ctypes.c_void_p),
+        ("h_stats", ctypes.c_void_p),
+        ("copy_stream", ctypes.c_void_p),
+        ("tables_stream", ctypes.c_void_p),
+        ("compute_stream", ctypes.c_void_p),
+        ("ev_wait", ctypes.c_void_p),
+        ("ev_copied", ctypes.c_void_p),
+        ("ev_tabled", ctypes.c_void_p),
+        ("ev_done", ctypes.c_void_p),
+        ("ws_needed", ctypes.POINTER(ctypes.c_size_t)),
+    ]
+
+
 # name -> (restype, argtypes); every symbol include/voxgrid_b200.h declares
 SIGNATURES = {
     "vg_workspace_layout": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.POINTER(VgWsLayout)]),
@@ -82,6 +100,9 @@ SIGNATURES = {
     "vg_slabs_f32": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                                     ctypes.c_void_p]),
+    "vg_submit_f32": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.POINTER(VgSubmitArgs),
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                     ctypes.c_void_p]),
     "vg_axis_tables_f32": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]),
     "vg_erf_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -101,7 +122,7 @@ SIGNATURES = {
     "vg_abi_version": (ctypes.c_int, []),
 }
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 _lib = None
 
 

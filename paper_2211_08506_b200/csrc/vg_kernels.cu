@@ -436,6 +436,7 @@ struct SlabParams {
   int stage_floats;     // floats of the staging area (sublists follow it)
   int c0_cap;           // level-0 candidate capacity (ints before the staging area)
   int fuse_channels;    // 1: one CTA serves every channel
+  int cta_order;        // per-channel CTAs: 0 molecule fastest, 1 channel fastest
   int tasks;            // tiles per (molecule, channel): y-chunks x row-blocks x z-blocks
   int n_molecules;
   int gx_win;           // staged gx rows per candidate (window), 0: all CTA rows
@@ -1079,12 +1080,20 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
       t = (int)(lin - b * (unsigned)p.tasks);
       T.b = b;
       T.c = 0;
-    } else {
+    } else if (p.cta_order == 0) {
       const unsigned nb = (unsigned)p.n_molecules;
       const unsigned rest = lin / nb;
       T.b = lin - rest * nb;
       const unsigned tt = rest / (unsigned)p.C;
       T.c = (int)(rest - tt * (unsigned)p.C);
+      t = (int)tt;
+    } else {
+      const unsigned nc = (unsigned)p.C;
+      const unsigned rest = lin / nc;
+      T.c = (int)(lin - rest * nc);
+      const unsigned nb = (unsigned)p.n_molecules;
+      const unsigned tt = rest / nb;
+      T.b = rest - tt * nb;
       t = (int)tt;
     }
   }
@@ -1831,6 +1840,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const size_t smem = (size_t)p.c0_cap * sizeof(int) + (size_t)p.stage_floats * sizeof(float) +
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
   p.fuse_channels = fuse ? 1 : 0;
+  p.cta_order = env_int("VG_ORDER", 0, 0, 1);
   p.tasks = p.n_jchunks * row_blocks * z_blocks;
   p.n_molecules = (int)d.n_molecules;
   const int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
@@ -1879,6 +1889,66 @@ VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
   if (rc != VG_OK || desc->n_molecules == 0) return rc;
   return launch_slabs(*desc, L, static_cast<char*>(workspace), out, stats,
                       static_cast<cudaStream_t>(stream));
+}
+
+VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, float* out,
+                         void* workspace, size_t workspace_bytes, vg_mol_stats* stats) {
+  if (a == nullptr) return set_error(VG_ERR_INVALID, "submit args are NULL");
+  vg_ws_layout L;
+  int rc = prepare(desc, out, workspace, workspace_bytes, &L);
+  if (rc == VG_ERR_WORKSPACE && a->ws_needed != nullptr) *a->ws_needed = L.total;
+  if (rc != VG_OK) return rc;
+  cudaStream_t cs = static_cast<cudaStream_t>(a->copy_stream);
+  cudaStream_t ts = static_cast<cudaStream_t>(a->tables_stream);
+  cudaStream_t ks = static_cast<cudaStream_t>(a->compute_stream);
+  cudaEvent_t ev_wait = static_cast<cudaEvent_t>(a->ev_wait);
+  cudaEvent_t ev_copied = static_cast<cudaEvent_t>(a->ev_copied);
+  cudaEvent_t ev_tabled = static_cast<cudaEvent_t>(a->ev_tabled);
+  cudaEvent_t ev_done = static_cast<cudaEvent_t>(a->ev_done);
+  if (ev_copied == nullptr || ev_tabled == nullptr || ev_done == nullptr)
+    return set_error(VG_ERR_INVALID, "submit events must be non-NULL");
+  const int64_t B = desc->n_molecules, n = desc->n_atoms;
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t r) {
+    if (e == cudaSuccess) e = r;
+    return e == cudaSuccess;
+  };
+  // slot reuse: every stage waits for the slot's previous consumer
+  if (ev_wait != nullptr) {
+    ok(cudaStreamWaitEvent(cs, ev_wait, 0));
+    ok(cudaStreamWaitEvent(ts, ev_wait, 0));
+    ok(cudaStreamWaitEvent(ks, ev_wait, 0));
+  }
+  if (a->h_offsets != nullptr && B > 0)
+    ok(cudaMemcpyAsync(const_cast<int64_t*>(desc->offsets), a->h_offsets, (size_t)(B + 1) * 8,
+                       cudaMemcpyHostToDevice, cs));
+  if (n > 0 && a->h_channel != nullptr)
+    ok(cudaMemcpyAsync(const_cast<int32_t*>(desc->channel), a->h_channel, (size_t)n * 4,
+                       cudaMemcpyHostToDevice, cs));
+  if (n > 0 && a->h_xyz != nullptr)
+    ok(cudaMemcpyAsync(const_cast<double*>(desc->xyz), a->h_xyz, (size_t)n * 24,
+                       cudaMemcpyHostToDevice, cs));
+  ok(cudaEventRecord(ev_copied, cs));
+  ok(cudaStreamWaitEvent(ts, ev_copied, 0));
+  if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (copy stage): %s", cudaGetErrorString(e));
+  char* ws = static_cast<char*>(workspace);
+  if (B > 0) {
+    rc = launch_tables(desc, L, ws, ts);
+    if (rc != VG_OK) return rc;
+  }
+  ok(cudaEventRecord(ev_tabled, ts));
+  ok(cudaStreamWaitEvent(ks, ev_tabled, 0));
+  if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (tables stage): %s", cudaGetErrorString(e));
+  if (B > 0) {
+    rc = launch_slabs(*desc, L, ws, out, stats, ks);
+    if (rc != VG_OK) return rc;
+    if (a->h_stats != nullptr && stats != nullptr)
+      ok(cudaMemcpyAsync(a->h_stats, stats, (size_t)B * sizeof(vg_mol_stats),
+                         cudaMemcpyDeviceToHost, ks));
+  }
+  ok(cudaEventRecord(ev_done, ks));
+  if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (compute stage): %s", cudaGetErrorString(e));
+  return VG_OK;
 }
 
 VG_API int vg_erf_f32(const float* t, float* out, int64_t n, void* stream) {

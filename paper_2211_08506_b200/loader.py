@@ -22,6 +22,7 @@ consumer-visible event.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -47,8 +48,12 @@ class _Slot:
         self.ws = None                            # K1 -> K3 tables
         self.out = None
         self.stats = None
-        self.done = None                          # K3 finished (inputs/ws/out reusable)
-        self.released = None                      # consumer's event (optional)
+        self.events = None                        # copied, tabled, done (cudaEvent_t)
+        self.args = None                          # vg_submit_args (reused)
+        self.desc = None                          # vg_batch_desc (geometry fixed)
+        self.ws_needed = ctypes.c_size_t(0)
+        self.used = False
+        self._host = None
 
 
 class GridPipeline:
@@ -84,8 +89,14 @@ class GridPipeline:
             t = torch.empty(max(need, 1), dtype=dtype, device=self.device)
         return t
 
-    def submit(self, offsets, channels, xyz, release=None) -> PipelineResult:
-        """Queue one CSR batch (numpy/torch, host or device). Returns at once."""
+    def submit(self, offsets, channels, xyz, release=None, stats_out=None) -> PipelineResult:
+        """Queue one CSR batch (numpy/torch, host or device). Returns at once.
+
+        One native call (``vg_submit_f32``) queues the H2D copies (copy
+        stream), K1 (tables stream) and K2/K3 (compute stream), ordered by the
+        slot's events. ``stats_out``: optional pinned host int64 (B, 2) tensor
+        that receives the per-grid stats (D2H on the compute stream, complete
+        at ``ready``)."""
         torch = self.torch
         spec = self.spec
         slot = self.slots[self.k % len(self.slots)]
@@ -93,64 +104,73 @@ class GridPipeline:
         B = int(len(offsets) - 1)
         n = int(len(channels))
         H, W, D = spec.shape
-        cs, ts, ks = self.copy_stream, self.tables_stream, self.compute_stream
-
-        # the slot's previous K3 must be done before its buffers are rewritten
-        for st in (cs, ts, ks):
-            if slot.done is not None:
-                st.wait_event(slot.done)
-            if release is not None:
+        if release is not None:
+            for st in (self.copy_stream, self.tables_stream, self.compute_stream):
                 st.wait_event(release)
-        if _on_device(offsets, torch.int64, self.device) and _on_device(
-                channels, torch.int32, self.device) and _on_device(xyz, torch.float64, self.device):
-            # device-resident inputs: used in place (caller keeps them unchanged until `ready`)
-            off_d, ch_d, xyz_d = offsets, channels, xyz.reshape(-1)
-            copied = None
+        if slot.events is None:
+            slot.events = [torch.cuda.Event() for _ in range(3)]   # copied, tabled, done
+            for ev in slot.events:   # torch creates the cudaEvent_t on first record
+                ev.record(self.compute_stream)
+            slot.args = _native.VgSubmitArgs()
+            slot.args.copy_stream = self.copy_stream.cuda_stream
+            slot.args.tables_stream = self.tables_stream.cuda_stream
+            slot.args.compute_stream = self.compute_stream.cuda_stream
+            slot.args.ev_copied = slot.events[0].cuda_event
+            slot.args.ev_tabled = slot.events[1].cuda_event
+            slot.args.ev_done = slot.events[2].cuda_event
+            slot.args.ws_needed = ctypes.pointer(slot.ws_needed)
+        args = slot.args
+        # the slot's previous K3 (and stats read-back) must be done before its
+        # buffers are rewritten (no wait on the slot's first use)
+        args.ev_wait = slot.events[2].cuda_event if slot.used else None
+        slot.used = True
+        if all(isinstance(t, torch.Tensor) and t.is_cuda for t in (offsets, channels, xyz)):
+            # device-resident inputs: used in place when they already have the
+            # kernel's dtypes (caller keeps them unchanged until `ready`)
+            off_d = offsets.to(self.device, torch.int64).contiguous()
+            ch_d = channels.to(self.device, torch.int32).contiguous()
+            xyz_d = xyz.to(self.device, torch.float64).contiguous().reshape(-1)
+            args.h_offsets = args.h_channel = args.h_xyz = None
+            host = (off_d, ch_d, xyz_d)
         else:
+            host = (_host_array(offsets, torch.int64), _host_array(channels, torch.int32),
+                    _host_array(xyz, torch.float64))
             slot.off = self._ensure(slot.off, B + 1, torch.int64)
             slot.ch = self._ensure(slot.ch, n, torch.int32)
             slot.xyz = self._ensure(slot.xyz, 3 * n, torch.float64)
-            with torch.cuda.stream(cs):
-                slot.off[:B + 1].copy_(torch.as_tensor(offsets), non_blocking=True)
-                if n:
-                    slot.ch[:n].copy_(torch.as_tensor(channels), non_blocking=True)
-                    slot.xyz[:3 * n].copy_(torch.as_tensor(xyz).reshape(-1), non_blocking=True)
-                copied = torch.cuda.Event()
-                copied.record(cs)
-            off_d, ch_d, xyz_d = slot.off[:B + 1], slot.ch[:n], slot.xyz[:3 * n]
+            off_d, ch_d, xyz_d = slot.off, slot.ch, slot.xyz
+            args.h_offsets = host[0].data_ptr()
+            args.h_channel = host[1].data_ptr() if n else None
+            args.h_xyz = host[2].data_ptr() if n else None
 
-        desc = self.engine.describe(off_d, ch_d, xyz_d.view(-1, 3), spec, mode=self.mode,
-                                    threshold=self.threshold)
-        layout = _native.VgWsLayout()
-        _native.check(self.lib.vg_workspace_layout(desc, layout), "vg_workspace_layout")
-        if slot.ws is None or slot.ws.numel() < layout.total:
-            slot.ws = torch.empty(max(layout.total, 1 << 20), dtype=torch.uint8,
-                                  device=self.device)
+        desc = slot.desc
+        if desc is None:
+            desc = slot.desc = self.engine.describe(off_d, ch_d, xyz_d.view(-1, 3), spec,
+                                                    mode=self.mode, threshold=self.threshold)
+        desc.n_molecules = B
+        desc.n_atoms = n
+        desc.offsets = off_d.data_ptr()
+        desc.channel = ch_d.data_ptr() if n else None
+        desc.xyz = xyz_d.data_ptr() if n else None
         shape = (B, spec.channels, H, W, D)
         if slot.out is None or tuple(slot.out.shape) != shape:
             slot.out = torch.empty(shape, dtype=torch.float32, device=self.device)
             slot.stats = torch.empty((B, 2), dtype=torch.int64, device=self.device)
-
-        # K1 on the tables stream (after the copy)
-        if copied is not None:
-            ts.wait_event(copied)
-        _native.check(self.lib.vg_axis_tables_f32(desc, slot.ws.data_ptr(), slot.ws.numel(),
-                                                  ts.cuda_stream), "vg_axis_tables_f32")
-        tabled = torch.cuda.Event()
-        tabled.record(ts)
-        # K3 on the compute stream (after K1)
-        ks.wait_event(tabled)
-        _native.check(self.lib.vg_slabs_f32(desc, slot.out.data_ptr(), slot.ws.data_ptr(),
-                                            slot.ws.numel(), slot.stats.data_ptr(),
-                                            ks.cuda_stream), "vg_slabs_f32")
-        done = torch.cuda.Event()
-        done.record(ks)
-        slot.done = done
+        args.h_stats = stats_out.data_ptr() if stats_out is not None else None
+        if slot.ws is None:
+            slot.ws = torch.empty(1 << 20, dtype=torch.uint8, device=self.device)
+        rc = self.lib.vg_submit_f32(desc, args, slot.out.data_ptr(), slot.ws.data_ptr(),
+                                    slot.ws.numel(), slot.stats.data_ptr())
+        if rc == _native.VG_ERR_WORKSPACE and slot.ws_needed.value > slot.ws.numel():
+            slot.ws = torch.empty(slot.ws_needed.value, dtype=torch.uint8, device=self.device)
+            rc = self.lib.vg_submit_f32(desc, args, slot.out.data_ptr(), slot.ws.data_ptr(),
+                                        slot.ws.numel(), slot.stats.data_ptr())
+        _native.check(rc, "vg_submit_f32")
         if B:
             self.launches += 2 if n else 1
-        # keep the input tensors alive until the copy has happened
-        slot._host = (offsets, channels, xyz)
-        return PipelineResult(slot.out, slot.stats, done, (self.k - 1) % len(self.slots))
+        # keep the inputs alive until the copy / kernels have read them
+        slot._host = host
+        return PipelineResult(slot.out, slot.stats, slot.events[2], (self.k - 1) % len(self.slots))
 
     def begin(self, event):
         """Make every stage wait for ``event`` (e.g. the start of a timed region)."""
@@ -162,11 +182,17 @@ class GridPipeline:
             st.synchronize()
 
 
-def _on_device(t, dtype, device) -> bool:
+def _host_array(a, dtype):
+    """A contiguous host tensor of `dtype` viewing (or converting) `a`."""
     import torch
 
-    return (isinstance(t, torch.Tensor) and t.is_cuda and t.device == device and t.dtype == dtype
-            and t.is_contiguous())
+    if isinstance(a, torch.Tensor):
+        t = a.cpu()
+    else:
+        t = torch.from_numpy(np.asarray(a))
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.reshape(-1).contiguous()
 
 
 def pinned_csr(offsets, channels, xyz):

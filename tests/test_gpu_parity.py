@@ -508,3 +508,27 @@ def test_pipeline_matches_serial_path():
     for g, st, g_ref, st_ref in outs:
         assert_bitwise(g, g_ref, "pipeline")
         assert np.array_equal(st, st_ref)
+
+
+def test_pipeline_back_to_back_with_stats_readback():
+    """Submissions queued without host syncs (depth-3 slots), host inputs as
+    pinned tensors and plain numpy, stats read back into pinned host memory
+    by the same native call: bits equal the serial path."""
+    from paper_2211_08506_b200.loader import GridPipeline, pinned_csr
+
+    cfg = synth.CONFIGS[4]
+    spec = spec_of(cfg)
+    batches = [synth.packed_batch(cfg, range(s, s + n)) for s, n in ((3, 9), (70, 4), (200, 11))]
+    pipe = GridPipeline(spec, depth=3)
+    res, st_host = [], []
+    for i, pb in enumerate(batches):
+        st_h = torch.empty((pb.n_molecules, 2), dtype=torch.int64).pin_memory()
+        inputs = pinned_csr(pb.offsets, pb.channels, pb.xyz) if i % 2 == 0 else (
+            pb.offsets, pb.channels, pb.xyz)
+        res.append(pipe.submit(*inputs, stats_out=st_h))
+        st_host.append(st_h)
+    pipe.synchronize()
+    for pb, r, st_h in zip(batches, res, st_host):
+        g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+        assert_bitwise(r.grids.cpu().numpy(), g_ref.cpu().numpy(), "pipeline b2b")
+        assert np.array_equal(st_h.numpy(), s_ref.cpu().numpy())

@@ -140,3 +140,26 @@ def test_saturated_erf_equals_full_erf(lib):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     nan = _host(lib.vg_erf_sat_f32_host, np.array([np.nan], np.float32))
     assert np.isnan(nan[0])
+
+
+def test_submit_validates_before_touching_the_gpu(lib):
+    """vg_submit_f32 rejects NULL args and reports the workspace it needs
+    before any CUDA call (so this runs without a GPU)."""
+    import ctypes
+
+    d = _native.VgBatchDesc()
+    d.n_molecules, d.n_atoms = 2, 5
+    d.offsets, d.xyz, d.channel = 16, 16, 16   # never dereferenced on these paths
+    d.delta[:] = (0.5, 0.5, 0.5)
+    d.scale = 1.0
+    d.H = d.W = d.D = 8
+    d.C = 3
+    d.threshold = float("nan")
+    assert lib.vg_submit_f32(d, None, 16, None, 0, None) == -1
+    need = ctypes.c_size_t(0)
+    args = _native.VgSubmitArgs()
+    args.ws_needed = ctypes.pointer(need)
+    assert lib.vg_submit_f32(d, args, 16, None, 0, None) == _native.VG_ERR_WORKSPACE
+    layout = _native.VgWsLayout()
+    assert lib.vg_workspace_layout(d, layout) == 0
+    assert need.value == layout.total > 0
