@@ -949,6 +949,134 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
   return nz;
 }
 
+// Slab pairs (YP = 2): each thread accumulates its slot on two adjacent
+// y-slabs (jj, jj+1) in one walk over the candidates active on either: one gx
+// and one gz load per candidate serve both slabs, gy is one 64-bit load. A
+// candidate active on only one slab of the pair reads gy = +0 on the other
+// (outside its y-support the table is +0), so its term there is
+// fl(fl(0*gx)*gz) = +0 and acc + (+0) = acc: every voxel still receives the
+// same terms in ascending atom order, bit for bit.
+__device__ __forceinline__ float2 lds_f32x2(unsigned a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
+template <typename Slot>
+__device__ __forceinline__ void walk_group_pair(unsigned act, int ent_x, unsigned gy_off, unsigned gxm,
+                                                unsigned gz_off, unsigned halfb, Slot& acc0,
+                                                Slot& acc1) {
+#ifdef VG_EXP_NOWALK
+  return;
+#endif
+  while (act != 0u) {
+    const int b0 = __ffs(act) - 1;
+    act &= act - 1u;
+    const bool two = act != 0u;   // warp-uniform
+    const int b1 = two ? __ffs(act) - 1 : b0;
+    if (two) act &= act - 1u;
+    const unsigned e0 = (unsigned)__shfl_sync(kFull, ent_x, b0);
+    const unsigned e1 = (unsigned)__shfl_sync(kFull, ent_x, b1);
+    const unsigned k0 = e0 & 0xFFFFFFu, k1 = e1 & 0xFFFFFFu;
+    Slot gz0, gz1;
+    lds_slot2(gz0, k0 + gz_off, halfb);
+    const float2 gy0 = lds_f32x2(k0 + gy_off);
+    const float gx0 = lds_f32(k0 - ((e0 >> 24) << 2) + gxm);
+    lds_slot2(gz1, k1 + gz_off, halfb);
+    const float2 gy1 = lds_f32x2(k1 + gy_off);
+    const float gx1 = lds_f32(k1 - ((e1 >> 24) << 2) + gxm);
+    add_scaled(acc0, VG_FMUL(gy0.x, gx0), gz0);   // ty (x) tx, then (x) tz, +=
+    add_scaled(acc1, VG_FMUL(gy0.y, gx0), gz0);
+    if (two) {
+      add_scaled(acc0, VG_FMUL(gy1.x, gx1), gz1);
+      add_scaled(acc1, VG_FMUL(gy1.y, gx1), gz1);
+    }
+  }
+}
+
+template <int M, int SW, bool FIRST>
+__device__ __noinline__ int accumulate_rows_pair(float* base, int64_t slab_elems, int m_stride,
+                                                 int nj, int ibase, int row_end, int R,
+                                                 Counts<M> cnt, unsigned lists_s, int cap,
+                                                 unsigned gx_off, unsigned gz_off, int half) {
+  using Slot = typename SlotW<SW>::T;
+  const unsigned halfb = 4u * (unsigned)half;
+  const int lane = (int)(threadIdx.x & 31);
+  bool small = M <= 2;
+  int2 pre[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    small = small && cnt.v[m] <= 32;
+    pre[m] = make_int2(0, 0);
+    if (M <= 2 && lane < cnt.v[m]) pre[m] = lds_int2(lists_s + 8u * (unsigned)(m * cap + lane));
+  }
+  int nz = 0;
+  float* dst_j = base;
+  for (int jj = 0; jj < nj; jj += 2, dst_j += 2 * slab_elems) {
+    const bool pair = jj + 1 < nj;   // uniform; an odd tail slab runs alone
+    const int jbits = (pair ? 3 : 1) << jj;
+    const unsigned gy_off = 4u * (unsigned)jj;   // 8-byte aligned: jj even, blocks 16-byte aligned
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const bool mine = ibase + m * R < row_end;
+      float* dst = dst_j + m * m_stride;
+      Slot acc0, acc1;
+      zero_slot(acc0);
+      zero_slot(acc1);
+      int before = 0;
+      if (!FIRST && mine) {
+        ld_slot(acc0, dst, half);
+        before = nonzeros_pos(acc0);
+        if (pair) {
+          ld_slot(acc1, dst + slab_elems, half);
+          before += nonzeros_pos(acc1);
+        }
+      }
+      const unsigned gxm = gx_off + 4u * (unsigned)(m * R);
+      bool touched;
+      if (small) {
+        const unsigned act = __ballot_sync(kFull, (pre[m].y & jbits) != 0);
+        touched = act != 0u;
+        walk_group_pair(act, pre[m].x, gy_off, gxm, gz_off, halfb, acc0, acc1);
+      } else {
+        touched = false;
+        const unsigned L = lists_s + 8u * (unsigned)(m * cap);
+        for (int c0 = 0; c0 < cnt.v[m]; c0 += 32) {
+          const int e = c0 + lane;
+          int2 ent = make_int2(0, 0);
+          if (e < cnt.v[m]) ent = lds_int2(L + 8u * (unsigned)e);
+          const unsigned act = __ballot_sync(kFull, (ent.y & jbits) != 0);
+          touched = touched || act != 0u;
+          walk_group_pair(act, ent.x, gy_off, gxm, gz_off, halfb, acc0, acc1);
+        }
+      }
+      if (mine) {
+        st_slot(dst, acc0, half);
+        int after = nonzeros_pos(acc0);
+        if (pair) {
+          st_slot(dst + slab_elems, acc1, half);
+          after += nonzeros_pos(acc1);
+        }
+        if (touched) nz += after - before;
+      }
+    }
+  }
+  return nz;
+}
+
+// Dispatch of the hot loop: single slabs (YP = 1) or slab pairs (YP = 2).
+template <int M, int SW, int YP, bool FIRST>
+__device__ __forceinline__ int accumulate(float* base, int64_t slab_elems, int m_stride, int nj,
+                                          int ibase, int row_end, int R, Counts<M> cnt,
+                                          unsigned lists_s, int cap, unsigned gx_off,
+                                          unsigned gz_off, int half) {
+  if (YP == 2)
+    return accumulate_rows_pair<M, SW, FIRST>(base, slab_elems, m_stride, nj, ibase, row_end, R,
+                                              cnt, lists_s, cap, gx_off, gz_off, half);
+  return accumulate_rows<M, SW, FIRST>(base, slab_elems, m_stride, nj, ibase, row_end, R, cnt,
+                                       lists_s, cap, gx_off, gz_off, half);
+}
+
 // Asynchronous global -> shared copies (LDGSTS): a warp issues every copy of
 // its candidates back to back instead of waiting on each load; completion is
 // awaited once (cp_async_wait_all) before the barrier that publishes them.
@@ -1056,7 +1184,7 @@ __device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* 
   }
 }
 
-template <int M, int SW>
+template <int M, int SW, int YP>
 __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotW<SW>::T;
   constexpr int kWidth = SW;
@@ -1155,7 +1283,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
         Counts<M> cnt;
         build_sublists<M>(p, sh.meta, n, c, lists, stage_s, j0, j1, T.row_base, rlo0, rhi0, R, cnt);
         __syncwarp();
-        nz += accumulate_rows<M, SW, true>(out_b + c * chan_elems, p.slab_elems, R * p.D, j1 - j0,
+        nz += accumulate<M, SW, YP, true>(out_b + c * chan_elems, p.slab_elems, R * p.D, j1 - j0,
                                            ibase, T.row_end, R, cnt, lists_s, p.stage_cap, gx_off,
                                            gz_off, half);
         __syncwarp();   // the next channel rewrites this warp's sublists
@@ -1217,11 +1345,11 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
           __syncthreads();  // staged tables visible to every warp (lists are warp-private)
 
           if (first)
-            nz += accumulate_rows<M, SW, true>(out_c + js * p.slab_elems + slot0, p.slab_elems,
+            nz += accumulate<M, SW, YP, true>(out_c + js * p.slab_elems + slot0, p.slab_elems,
                                                 R * p.D, je - js, ibase, T.row_end, R, cnt,
                                                 lists_s, p.stage_cap, gx_off, gz_off, half);
           else
-            nz += accumulate_rows<M, SW, false>(out_c + js * p.slab_elems + slot0, p.slab_elems,
+            nz += accumulate<M, SW, YP, false>(out_c + js * p.slab_elems + slot0, p.slab_elems,
                                                  R * p.D, je - js, ibase, T.row_end, R, cnt,
                                                  lists_s, p.stage_cap, gx_off, gz_off, half);
           __syncthreads();  // the next segment / sub-chunk rewrites the staging area
@@ -1536,38 +1664,38 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   return true;
 }
 
-template <int M, int SW>
+template <int M, int SW, int YP>
 void launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   // The row kernel is register-limited to 4 CTAs/SM; ask for the largest
   // shared-memory carveout so that shared memory never lowers that.
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(vg_slab_kernel<M, SW>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(vg_slab_kernel<M, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          96 * 1024);
     configured = true;
   }
-  vg_slab_kernel<M, SW><<<grid, nt, smem, st>>>(p);
+  vg_slab_kernel<M, SW, YP><<<grid, nt, smem, st>>>(p);
 }
 
-template <int SW>
+template <int SW, int YP>
 void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   switch (M) {
-    case 1: launch_rows_m<1, SW>(grid, nt, smem, st, p); break;
-    case 2: launch_rows_m<2, SW>(grid, nt, smem, st, p); break;
-    case 3: launch_rows_m<3, SW>(grid, nt, smem, st, p); break;
-    case 4: launch_rows_m<4, SW>(grid, nt, smem, st, p); break;
-    case 5: launch_rows_m<5, SW>(grid, nt, smem, st, p); break;
-    case 6: launch_rows_m<6, SW>(grid, nt, smem, st, p); break;
-    case 7: launch_rows_m<7, SW>(grid, nt, smem, st, p); break;
-    default: launch_rows_m<8, SW>(grid, nt, smem, st, p); break;
+    case 1: launch_rows_m<1, SW, YP>(grid, nt, smem, st, p); break;
+    case 2: launch_rows_m<2, SW, YP>(grid, nt, smem, st, p); break;
+    case 3: launch_rows_m<3, SW, YP>(grid, nt, smem, st, p); break;
+    case 4: launch_rows_m<4, SW, YP>(grid, nt, smem, st, p); break;
+    case 5: launch_rows_m<5, SW, YP>(grid, nt, smem, st, p); break;
+    case 6: launch_rows_m<6, SW, YP>(grid, nt, smem, st, p); break;
+    case 7: launch_rows_m<7, SW, YP>(grid, nt, smem, st, p); break;
+    default: launch_rows_m<8, SW, YP>(grid, nt, smem, st, p); break;
   }
 }
 
 // Registers per thread of the row kernel instance (queried once): the
 // shared-memory budget keeps as many CTAs resident as the registers allow.
-template <int SW>
+template <int SW, int YP>
 int rows_regs_sw(int M) {
   static int regs[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int m = M < 1 ? 1 : (M > 8 ? 8 : M);
@@ -1575,22 +1703,23 @@ int rows_regs_sw(int M) {
     cudaFuncAttributes a;
     cudaError_t e = cudaErrorInvalidValue;
     switch (m) {
-      case 1: e = cudaFuncGetAttributes(&a, vg_slab_kernel<1, SW>); break;
-      case 2: e = cudaFuncGetAttributes(&a, vg_slab_kernel<2, SW>); break;
-      case 3: e = cudaFuncGetAttributes(&a, vg_slab_kernel<3, SW>); break;
-      case 4: e = cudaFuncGetAttributes(&a, vg_slab_kernel<4, SW>); break;
-      case 5: e = cudaFuncGetAttributes(&a, vg_slab_kernel<5, SW>); break;
-      case 6: e = cudaFuncGetAttributes(&a, vg_slab_kernel<6, SW>); break;
-      case 7: e = cudaFuncGetAttributes(&a, vg_slab_kernel<7, SW>); break;
-      default: e = cudaFuncGetAttributes(&a, vg_slab_kernel<8, SW>); break;
+      case 1: e = cudaFuncGetAttributes(&a, vg_slab_kernel<1, SW, YP>); break;
+      case 2: e = cudaFuncGetAttributes(&a, vg_slab_kernel<2, SW, YP>); break;
+      case 3: e = cudaFuncGetAttributes(&a, vg_slab_kernel<3, SW, YP>); break;
+      case 4: e = cudaFuncGetAttributes(&a, vg_slab_kernel<4, SW, YP>); break;
+      case 5: e = cudaFuncGetAttributes(&a, vg_slab_kernel<5, SW, YP>); break;
+      case 6: e = cudaFuncGetAttributes(&a, vg_slab_kernel<6, SW, YP>); break;
+      case 7: e = cudaFuncGetAttributes(&a, vg_slab_kernel<7, SW, YP>); break;
+      default: e = cudaFuncGetAttributes(&a, vg_slab_kernel<8, SW, YP>); break;
     }
     regs[m] = e == cudaSuccess && a.numRegs > 0 ? a.numRegs : 64;
   }
   return regs[m];
 }
 
-int rows_regs(int sw, int M) {
-  return sw == 8 ? rows_regs_sw<8>(M) : (sw == 4 ? rows_regs_sw<4>(M) : rows_regs_sw<1>(M));
+int rows_regs(int sw, int yp, int M) {
+  if (sw == 8) return yp == 2 ? rows_regs_sw<8, 2>(M) : rows_regs_sw<8, 1>(M);
+  return sw == 4 ? rows_regs_sw<4, 1>(M) : rows_regs_sw<1, 1>(M);
 }
 
 // z window (slots per row segment) of the row kernel: whole rows up to 16
@@ -1703,6 +1832,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   plan_slabs(d, aligned16, &P);
   const int64_t slab = (int64_t)d.W * d.D;
   const int sw = P.sw, zw = P.zw, width = P.width, spr = P.spr;
+  // hot loop over single slabs or slab pairs (8-voxel slots only)
+  const int yp = sw == 8 && env_int("VG_YP", 2, 1, 2) == 2 ? 2 : 1;
   int nt = P.nt;
   const int R = P.R, M = P.M, row_blocks = P.row_blocks;
 
@@ -1818,7 +1949,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   // when a molecule has more than 2*blockDim atoms); with K2 bins the CTA's
   // bin is its candidate source. Capacity in ints, 16-byte aligned.
   p.c0_cap = p.bins != nullptr ? 0 : (mean_atoms > 64 ? kC0CapMax : 256);
-  p.c0_cap = env_int("VG_C0", p.c0_cap, 0, kC0CapMax);
+  p.c0_cap = round_up4(env_int("VG_C0", p.c0_cap, 0, kC0CapMax));   // keeps staging 16-byte aligned
   // Staging capacity: what the batch's molecules need (about 2x the mean atom
   // count, at most kListCap), within the shared memory that keeps the
   // register-limited number of CTAs resident per SM (228 KB per SM, 1 KB
@@ -1826,7 +1957,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   int cap_max = kListCap;
   cap_max = env_int("VG_CAP_MAX", cap_max, 1, kListCap);
   const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > cap_max ? cap_max : mean_atoms * 2));
-  const int regs = (rows_regs(sw, M) + 7) & ~7;   // allocation granularity
+  const int regs = (rows_regs(sw, yp, M) + 7) & ~7;   // allocation granularity
   const int reg_blocks = max(1, min(2048 / nt, 65536 / (regs * nt)));
   const int64_t budget = (int64_t)228 * 1024 / reg_blocks - 1024 - (int64_t)sizeof(SlabShared) -
                          (int64_t)p.c0_cap * 4 - (int64_t)(M * R + 8 + 3) * 4;
@@ -1846,12 +1977,14 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
   if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
   const dim3 grid((unsigned)ctas);
-  if (sw == 8)
-    launch_rows<8>(M, grid, nt, smem, st, p);
+  if (sw == 8 && yp == 2)
+    launch_rows<8, 2>(M, grid, nt, smem, st, p);
+  else if (sw == 8)
+    launch_rows<8, 1>(M, grid, nt, smem, st, p);
   else if (sw == 4)
-    launch_rows<4>(M, grid, nt, smem, st, p);
+    launch_rows<4, 1>(M, grid, nt, smem, st, p);
   else
-    launch_rows<1>(M, grid, nt, smem, st, p);
+    launch_rows<1, 1>(M, grid, nt, smem, st, p);
   return check_launch("vg_slab_kernel");
 }
 

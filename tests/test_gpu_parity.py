@@ -532,3 +532,27 @@ def test_pipeline_back_to_back_with_stats_readback():
         g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
         assert_bitwise(r.grids.cpu().numpy(), g_ref.cpu().numpy(), "pipeline b2b")
         assert np.array_equal(st_h.numpy(), s_ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("yp", ["1", "2"])
+def test_slab_pair_hot_loop_variants(monkeypatch, yp):
+    """Both hot loops (single slabs, slab pairs: VG_YP) are bit-exact: golden
+    grids (odd slab counts, periodic, thresholds), the segmented overflow
+    path (continued sums), K2 bins, fused and per-channel CTAs."""
+    monkeypatch.setenv("VG_YP", yp)
+    for m, g in grid_cases():
+        lattice = vg.LatticeCell(tuple(m["periodic"])) if m["periodic"] else None
+        spec = vg.GridSpec(tuple(m["shape"]), m["channels"],
+                           vg.BoundingBox(tuple(m["origin"]), tuple(m["extents"])), m["sigma"],
+                           lattice)
+        ps = vg.ParticleSet(np.array(m["chans"], dtype=np.int64),
+                            np.array(m["pos"]).reshape(-1, 3), lattice)
+        grid, st = vg.generate_grid(ps, spec, mode=m["mode"], threshold=m["threshold"])
+        assert_bitwise(grid.numpy(), g, m["name"])
+        assert st.nonzero_voxels == m["nonzero_voxels"]
+    test_candidate_list_overflow_path_vs_oracle()
+    _compare_with_oracle(synth.CONFIGS[1], range(0, 1024, 9))
+    _compare_with_oracle(synth.CONFIGS[4], range(0, 4096, 37))
+    _compare_with_oracle(synth.CONFIGS[3], [5, 17])
+    monkeypatch.setenv("VG_FUSE", "0")
+    _compare_with_oracle(synth.CONFIGS[0], range(64))
