@@ -940,10 +940,8 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
           walk_group(act, ent.x, gy_off, gxm, gz_off, halfb, acc);
         }
       }
-      if (mine) {
-        st_slot(dst, acc, half);
-        if (touched) nz += nonzeros_pos(acc) - before;
-      }
+      if (mine) st_slot(dst, acc, half);
+      if (__any_sync(kFull, touched) && mine) nz += nonzeros_pos(acc) - before;
     }
   }
   return nz;
@@ -1052,13 +1050,12 @@ __device__ __noinline__ int accumulate_rows_pair(float* base, int64_t slab_elems
       }
       if (mine) {
         st_slot(dst, acc0, half);
-        int after = nonzeros_pos(acc0);
-        if (pair) {
-          st_slot(dst + slab_elems, acc1, half);
-          after += nonzeros_pos(acc1);
-        }
-        if (touched) nz += after - before;
+        if (pair) st_slot(dst + slab_elems, acc1, half);
       }
+      // counted only where some candidate was active (a vote: a real branch,
+      // not a predicated count, on the many untouched pairs)
+      if (__any_sync(kFull, touched) && mine)
+        nz += nonzeros_pos(acc0) + (pair ? nonzeros_pos(acc1) : 0) - before;
     }
   }
   return nz;
@@ -1184,6 +1181,21 @@ __device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* 
   }
 }
 
+#ifdef VG_EXP_TIMING
+// Experiment builds only (-DVG_EXP_TIMING): per-CTA phase timestamps.
+__device__ unsigned long long g_vg_ts[1 << 17][8];
+__device__ __forceinline__ unsigned long long vg_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define VG_TS(i) do { if (threadIdx.x == 0 && blockIdx.x < (1u << 17)) g_vg_ts[blockIdx.x][i] = vg_gtime(); } while (0)
+#define VG_TSV(i, v) do { if (threadIdx.x == 0 && blockIdx.x < (1u << 17)) g_vg_ts[blockIdx.x][i] = (v); } while (0)
+#else
+#define VG_TS(i) do { } while (0)
+#define VG_TSV(i, v) do { } while (0)
+#endif
+
 template <int M, int SW, int YP>
 __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotW<SW>::T;
@@ -1263,7 +1275,9 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   const int rlo0 = T.row_base + T.wr0, rhi0 = T.row_base + T.wr1;
   const int64_t chan_elems = (int64_t)p.H * p.slab_elems;
 
+  VG_TS(0);
   int nz = 0;
+  int rounds = 0, staged = 0;
   int c_lo = T.c, c_hi = T.c + 1;
   if (p.fuse_channels) {
     // Every channel from one candidate list and one staging pass, when the
@@ -1319,6 +1333,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
       src_begin = n0 >= 0 ? 0 : T.a0;
       src_end = n0 >= 0 ? n0 : T.a1;
     }
+    VG_TS(1);
     int js = j0, sc = j1 - j0;
     while (js < j1) {
       const int je = min(j1, js + sc);
@@ -1343,6 +1358,9 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
           build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, T.row_base, rlo0, rhi0, R, cnt);
           cp_async_wait_all();
           __syncthreads();  // staged tables visible to every warp (lists are warp-private)
+          if (rounds == 0) VG_TS(2);
+          ++rounds;
+          staged += ns;
 
           if (first)
             nz += accumulate<M, SW, YP, true>(out_c + js * p.slab_elems + slot0, p.slab_elems,
@@ -1352,6 +1370,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
             nz += accumulate<M, SW, YP, false>(out_c + js * p.slab_elems + slot0, p.slab_elems,
                                                  R * p.D, je - js, ibase, T.row_end, R, cnt,
                                                  lists_s, p.stage_cap, gx_off, gz_off, half);
+          VG_TS(3);
           __syncthreads();  // the next segment / sub-chunk rewrites the staging area
           first = false;
         }
@@ -1363,6 +1382,14 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   }
   if (p.stats != nullptr)
     finish_stats(p, sh, T.b, T.a0, T.a1, nz, T.c == 0 && chunk == 0 && rblk == 0 && zblk == 0);
+#ifdef VG_EXP_TIMING
+  VG_TS(4);
+  unsigned smid;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+  VG_TSV(5, ((unsigned long long)smid << 32) | (unsigned)T.c);
+  VG_TSV(6, ((unsigned long long)rounds << 32) | (unsigned)staged);
+  VG_TSV(7, ((unsigned long long)T.b << 32) | (unsigned)(chunk * 256 + rblk * 16 + zblk));
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -2113,6 +2140,13 @@ VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
   if (tail > 0) vg_fill_tail_kernel<<<1, 32, 0, st>>>(out + n4 * 4, tail, value);
   return check_launch("vg_fill_kernel");
 }
+
+#ifdef VG_EXP_TIMING
+VG_API int vg_exp_timing_fetch(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_vg_ts, bytes < sizeof(g_vg_ts) ? bytes : sizeof(g_vg_ts)) ==
+                 cudaSuccess ? VG_OK : VG_ERR_CUDA;
+}
+#endif
 
 VG_API int vg_exp_f32_host(const float* x, float* out, size_t n) {
   if (n > 0 && (x == nullptr || out == nullptr)) return set_error(VG_ERR_INVALID, "NULL pointer");
