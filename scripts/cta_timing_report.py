@@ -1,6 +1,8 @@
+"""Per-CTA phase report of K3 from scripts/cta_timing.py output:
+python scripts/cta_timing_report.py <ts.npy> <number of CTAs of the launch>"""
 import numpy as np, sys
-cfgn=sys.argv[1]; n=int(sys.argv[2])
-a=np.load(f'/root/repo/gpurun_out/ts_cfg{cfgn}.npy')[:n].astype(np.int64)
+n=int(sys.argv[2])
+a=np.load(sys.argv[1])[:n].astype(np.int64)
 t0=a[:,0]; base=t0.min()
 t0=t0-base; t1=a[:,1]-base; t2=a[:,2]-base; t3=a[:,3]-base; t4=a[:,4]-base
 sm=a[:,5]>>32; c=a[:,5]&0xffffffff; rounds=a[:,6]>>32; staged=a[:,6]&0xffffffff

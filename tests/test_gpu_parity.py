@@ -556,3 +556,24 @@ def test_slab_pair_hot_loop_variants(monkeypatch, yp):
     _compare_with_oracle(synth.CONFIGS[3], [5, 17])
     monkeypatch.setenv("VG_FUSE", "0")
     _compare_with_oracle(synth.CONFIGS[0], range(64))
+
+
+def test_fused_cta_fallback_on_large_molecules_vs_oracle(monkeypatch):
+    """Channel-fused CTAs on molecules too large for one staging pass fall
+    back to the per-channel path (halved sub-chunks, segmented slabs);
+    VG_FUSE=1 forces fused CTAs on these sizes."""
+    monkeypatch.setenv("VG_FUSE", "1")
+    rng = np.random.default_rng(2024)
+    sizes = [3, 150, 400, 0, 60, 900, 210]
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(offsets[-1])
+    xyz = rng.uniform(0.0, 10.0, (n, 3))
+    ch = rng.choice(4, size=n, p=[0.5, 0.3, 0.15, 0.05]).astype(np.int32)
+    shape = (40, 36, 48)
+    spec = vg.GridSpec(shape, 4, vg.BoundingBox((0, 0, 0), (10.0, 10.0, 10.0)), 0.5)
+    grids, st = vg.generate_packed(offsets, ch, xyz, spec)
+    ref, rs = orc.batch(offsets, ch, xyz, orc.Geometry(shape, 4, (0, 0, 0), (10.0, 10.0, 10.0), 0.5),
+                        workers=orc.host_cores())
+    assert_bitwise(grids.cpu().numpy(), ref, "fused halving")
+    assert [int(v) for v in st[:, 0].cpu()] == [r["voxel_writes"] for r in rs]
+    assert [int(v) for v in st[:, 1].cpu()] == [r["nonzero_voxels"] for r in rs]
