@@ -119,6 +119,7 @@ typedef struct vg_submit_args {
   void* ev_tabled;
   void* ev_done;
   size_t* ws_needed;
+  int32_t* kernels;        /* out (if non-NULL): kernels this call launched (K1, K2, K3) */
 } vg_submit_args;
 
 int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* args, float* out,

@@ -88,6 +88,7 @@ class VgSubmitArgs(ctypes.Structure):
         ("ev_tabled", ctypes.c_void_p),
         ("ev_done", ctypes.c_void_p),
         ("ws_needed", ctypes.POINTER(ctypes.c_size_t)),
+        ("kernels", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 

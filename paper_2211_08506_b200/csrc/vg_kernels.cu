@@ -1853,7 +1853,7 @@ bool bin_plan(const vg_batch_desc& d, int* jc, int* nch) {
 
 // K3 launch (tables must already be in the workspace, same stream).
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
-                 vg_mol_stats* stats, cudaStream_t st) {
+                 vg_mol_stats* stats, cudaStream_t st, int* kernels = nullptr) {
   const bool aligned16 = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   SlabPlan P;
   plan_slabs(d, aligned16, &P);
@@ -1911,6 +1911,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
       vg_slab_generic_kernel<true><<<(unsigned)tasks, nt, 0, st>>>(p);
     else
       vg_slab_generic_kernel<false><<<(unsigned)tasks, nt, 0, st>>>(p);
+    if (kernels != nullptr) *kernels += 1;
     return check_launch("vg_slab_generic_kernel");
   }
 
@@ -1945,6 +1946,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
       configured = true;
     }
     vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
+    if (kernels != nullptr) *kernels += 1;
     const int rc = check_launch("vg_bin_kernel");
     if (rc != VG_OK) return rc;
   }
@@ -2012,6 +2014,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     launch_rows<4, 1>(M, grid, nt, smem, st, p);
   else
     launch_rows<1, 1>(M, grid, nt, smem, st, p);
+  if (kernels != nullptr) *kernels += 1;
   return check_launch("vg_slab_kernel");
 }
 
@@ -2092,15 +2095,17 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   ok(cudaStreamWaitEvent(ts, ev_copied, 0));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (copy stage): %s", cudaGetErrorString(e));
   char* ws = static_cast<char*>(workspace);
-  if (B > 0) {
+  int kernels = 0;
+  if (B > 0 && n > 0) {
     rc = launch_tables(desc, L, ws, ts);
     if (rc != VG_OK) return rc;
+    kernels = 1;
   }
   ok(cudaEventRecord(ev_tabled, ts));
   ok(cudaStreamWaitEvent(ks, ev_tabled, 0));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (tables stage): %s", cudaGetErrorString(e));
   if (B > 0) {
-    rc = launch_slabs(*desc, L, ws, out, stats, ks);
+    rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels);
     if (rc != VG_OK) return rc;
     if (a->h_stats != nullptr && stats != nullptr)
       ok(cudaMemcpyAsync(a->h_stats, stats, (size_t)B * sizeof(vg_mol_stats),
@@ -2108,6 +2113,7 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   }
   ok(cudaEventRecord(ev_done, ks));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (compute stage): %s", cudaGetErrorString(e));
+  if (a->kernels != nullptr) *a->kernels = kernels;
   return VG_OK;
 }
 

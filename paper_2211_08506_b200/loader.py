@@ -52,6 +52,7 @@ class _Slot:
         self.args = None                          # vg_submit_args (reused)
         self.desc = None                          # vg_batch_desc (geometry fixed)
         self.ws_needed = ctypes.c_size_t(0)
+        self.kernels = ctypes.c_int32(0)           # kernels the last submit launched
         self.used = False
         self._host = None
 
@@ -119,6 +120,7 @@ class GridPipeline:
             slot.args.ev_tabled = slot.events[1].cuda_event
             slot.args.ev_done = slot.events[2].cuda_event
             slot.args.ws_needed = ctypes.pointer(slot.ws_needed)
+            slot.args.kernels = ctypes.pointer(slot.kernels)
         args = slot.args
         # the slot's previous K3 (and stats read-back) must be done before its
         # buffers are rewritten (no wait on the slot's first use)
@@ -166,8 +168,7 @@ class GridPipeline:
             rc = self.lib.vg_submit_f32(desc, args, slot.out.data_ptr(), slot.ws.data_ptr(),
                                         slot.ws.numel(), slot.stats.data_ptr())
         _native.check(rc, "vg_submit_f32")
-        if B:
-            self.launches += 2 if n else 1
+        self.launches += slot.kernels.value   # K1, K2 (binned batches), K3
         # keep the inputs alive until the copy / kernels have read them
         slot._host = host
         return PipelineResult(slot.out, slot.stats, slot.events[2], (self.k - 1) % len(self.slots))
