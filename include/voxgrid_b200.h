@@ -149,6 +149,39 @@ int vg_mse_f64(const float* ref, const float* grids, int64_t n_voxels, int32_t n
 int vg_loss_gradient_f64(const vg_batch_desc* desc, const float* ref, const float* regen,
                          double* grad, void* stream);
 
+/* Device-resident descent of refine_coords (reversal.py:325-398): the loop
+ * state lives in device memory so that an iteration (gradient, candidates,
+ * batched regeneration, batched loss, selection) needs no host round trip;
+ * the host reads `done` every few iterations. Once `done` is set, both calls
+ * leave the state, positions and regen untouched. */
+typedef struct vg_descent_state {
+  double current;       /* loss at the current positions                        */
+  double best;          /* lowest loss seen (its positions are in best_pos)     */
+  int64_t iterations;   /* accepted steps                                       */
+  int64_t forced;       /* consecutive steps with no candidate <= current       */
+  int32_t done;         /* a stop rule fired                                    */
+  int32_t diverged;     /* stopped after `patience` forced steps                */
+  int32_t sel;          /* last selected candidate (internal)                   */
+  int32_t moved;        /* last select call took a step (internal)              */
+} vg_descent_state;
+
+/* Loop top: done if iterations >= max_iters or current < tolerance, or if
+ * the gradient is all zero; otherwise cands[g] = pos - steps[g] * grad for
+ * g < n_steps (fp64, unfused: the reference's positions - (step0*h)*grad).
+ * n_coords = 3 * atoms. */
+int vg_descent_candidates_f64(vg_descent_state* state, const double* pos, const double* grad,
+                              const double* steps, double* cands, int32_t n_coords,
+                              int32_t n_steps, int64_t max_iters, double tolerance, void* stream);
+
+/* After the candidates' losses: take the first g with losses[g] <= current
+ * (else the last, smallest step), move pos and regen (grids[g], n_voxels
+ * floats) to it, count the step, track the best, and stop after `patience`
+ * consecutive forced steps. */
+int vg_descent_select_f64(vg_descent_state* state, const double* losses, const double* cands,
+                          const float* grids, int32_t n_coords, int32_t n_steps,
+                          int64_t n_voxels, int32_t patience, double* pos, double* best_pos,
+                          float* regen, void* stream);
+
 /* Device fill with 128-bit stores (HBM write-bandwidth probe for the roofline). */
 int vg_fill_f32(float* out, int64_t n, float value, void* stream);
 

@@ -92,6 +92,19 @@ class VgSubmitArgs(ctypes.Structure):
     ]
 
 
+class VgDescentState(ctypes.Structure):
+    _fields_ = [
+        ("current", ctypes.c_double),
+        ("best", ctypes.c_double),
+        ("iterations", ctypes.c_int64),
+        ("forced", ctypes.c_int64),
+        ("done", ctypes.c_int32),
+        ("diverged", ctypes.c_int32),
+        ("sel", ctypes.c_int32),
+        ("moved", ctypes.c_int32),
+    ]
+
+
 # name -> (restype, argtypes); every symbol include/voxgrid_b200.h declares
 SIGNATURES = {
     "vg_workspace_layout": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.POINTER(VgWsLayout)]),
@@ -116,6 +129,14 @@ SIGNATURES = {
                                   ctypes.c_void_p]),
     "vg_loss_gradient_f64": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "vg_descent_candidates_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                                 ctypes.c_int32, ctypes.c_int64, ctypes.c_double,
+                                                 ctypes.c_void_p]),
+    "vg_descent_select_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "vg_exp_f32_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "vg_erf_f32_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "vg_erf_sat_f32_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),

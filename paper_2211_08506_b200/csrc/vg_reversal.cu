@@ -35,7 +35,7 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMseBlocks = 296;     // partial sums per grid (2 x 148 SMs)
 constexpr int kMseThreads = 256;
-constexpr int kGradThreads = 256;
+constexpr int kGradThreads = 512;
 constexpr int kGradMaxAxis = 1024;  // per-axis table length staged in shared memory
 
 int fail(int code, const char* what, cudaError_t e) {
@@ -160,38 +160,163 @@ __global__ void __launch_bounds__(kGradThreads) vg_grad_kernel(const __grid_cons
     }
   }
   __syncthreads();
+  // One pass over the union of the three axis boxes (derivative support on
+  // the axis, value supports on the other two): each voxel's difference is
+  // read once and feeds all three sums. Outside an axis' box one of its
+  // factors is exactly +0, so the extra terms add nothing (d is finite).
   const int64_t slab = (int64_t)p.W * p.D;
   const float* ref_c = p.ref + (int64_t)c * p.H * slab;
   const float* reg_c = p.regen + (int64_t)c * p.H * slab;
+  int lo[3], ext[3];
+  bool empty = false;
+  for (int q = 0; q < 3; ++q) {
+    const bool v_ok = vsup[q][1] > vsup[q][0], g_ok = gsup[q][1] > gsup[q][0];
+    empty = empty || !(v_ok || g_ok);
+    const int l = !v_ok ? gsup[q][0] : (!g_ok ? vsup[q][0] : min(vsup[q][0], gsup[q][0]));
+    const int h = !v_ok ? gsup[q][1] : (!g_ok ? vsup[q][1] : max(vsup[q][1], gsup[q][1]));
+    lo[q] = l;
+    ext[q] = h - l;
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (!empty) {
+    const int nx = ext[0], ny = ext[1], nz = ext[2];
+    const int total = nx * ny * nz;   // <= 1024^3 / 8 within one support box
+    for (int v = threadIdx.x; v < total; v += blockDim.x) {
+      const int r = v / nz;
+      const int k = lo[2] + (v - r * nz);
+      const int j = lo[1] + r / nx;
+      const int i = lo[0] + (r - (r / nx) * nx);
+      const int64_t off = (int64_t)j * slab + (int64_t)i * p.D + k;
+      const double d = (double)reg_c[off] - (double)ref_c[off];
+      const double vx = val[0][i], vy = val[1][j], vz = val[2][k];
+      acc[0] += d * (double)der[0][i] * vy * vz;
+      acc[1] += d * vx * (double)der[1][j] * vz;
+      acc[2] += d * vx * vy * (double)der[2][k];
+    }
+  }
   for (int axis = 0; axis < 3; ++axis) {
-    int lo[3], hi[3];
-    for (int q = 0; q < 3; ++q) {
-      lo[q] = q == axis ? gsup[q][0] : vsup[q][0];
-      hi[q] = q == axis ? gsup[q][1] : vsup[q][1];
-    }
-    double acc = 0.0;
-    const int nx = hi[0] - lo[0], ny = hi[1] - lo[1], nz = hi[2] - lo[2];
-    if (nx > 0 && ny > 0 && nz > 0 && gsup[axis][1] > gsup[axis][0]) {
-      const float* fx = axis == 0 ? der[0] : val[0];
-      const float* fy = axis == 1 ? der[1] : val[1];
-      const float* fz = axis == 2 ? der[2] : val[2];
-      const int64_t total = (int64_t)nx * ny * nz;
-      for (int64_t v = threadIdx.x; v < total; v += blockDim.x) {
-        const int k = lo[2] + (int)(v % nz);
-        const int64_t r = v / nz;
-        const int i = lo[0] + (int)(r % nx);
-        const int j = lo[1] + (int)(r / nx);
-        const int64_t off = (int64_t)j * slab + (int64_t)i * p.D + k;
-        const double d = (double)reg_c[off] - (double)ref_c[off];
-        acc += d * (double)fx[i] * (double)fy[j] * (double)fz[k];
-      }
-    }
-    const double t = block_reduce_f64(acc, red);
+    const double t = block_reduce_f64(acc[axis], red);
     if (threadIdx.x == 0) p.grad[a * 3 + axis] = p.inv_n2 * t;
   }
 }
 
+// --- device-resident descent (refine_coords, reversal.py:325-398) ----------
+// One CTA: the loop-top stop rules, then the backoff candidates.
+__global__ void vg_descent_cand_kernel(vg_descent_state* st, const double* __restrict__ pos,
+                                       const double* __restrict__ grad,
+                                       const double* __restrict__ steps, double* __restrict__ cands,
+                                       int nc, int G, long long max_iters, double tol) {
+  __shared__ int any_nz;
+  if (threadIdx.x == 0) any_nz = 0;
+  __syncthreads();
+  if (st->done) return;   // uniform
+  // `while iterations < max_iters`, `if current < tolerance: break`
+  bool stop = st->iterations >= max_iters || st->current < tol;
+  if (!stop) {
+    bool nz = false;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) nz = nz || grad[i] != 0.0;
+    if (nz) any_nz = 1;
+  }
+  __syncthreads();
+  stop = stop || any_nz == 0;   // `if not np.any(grad): break`
+  if (stop) {
+    if (threadIdx.x == 0) st->done = 1;
+    return;
+  }
+  for (int i = threadIdx.x; i < G * nc; i += blockDim.x) {
+    const int g = i / nc, k = i - g * nc;
+    cands[i] = __dsub_rn(pos[k], __dmul_rn(steps[g], grad[k]));   // pos - (step0*h)*grad
+  }
+}
+
+// One CTA: first candidate (in halving order) whose loss does not exceed the
+// current one, else the smallest step; state update in the reference's order.
+__global__ void vg_descent_select_kernel(vg_descent_state* st, const double* __restrict__ losses,
+                                         const double* __restrict__ cands, int nc, int G,
+                                         int patience, double* __restrict__ pos,
+                                         double* __restrict__ best_pos) {
+  const bool done = st->done != 0;
+  __syncthreads();
+  if (done) {
+    if (threadIdx.x == 0) st->moved = 0;
+    return;
+  }
+  const double cur = st->current;
+  int s = G - 1;
+  bool ok_any = false;
+  for (int g = 0; g < G; ++g) {
+    if (losses[g] <= cur) {
+      s = g;
+      ok_any = true;
+      break;
+    }
+  }
+  const double next = losses[s];
+  const bool better = next < st->best;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const double v = cands[(size_t)s * nc + i];
+    pos[i] = v;
+    if (better) best_pos[i] = v;
+  }
+  __syncthreads();   // every thread has read the state
+  if (threadIdx.x == 0) {
+    st->current = next;
+    st->iterations += 1;
+    st->forced = ok_any ? 0 : st->forced + 1;
+    if (better) st->best = next;
+    if (st->forced >= patience) {
+      st->diverged = 1;
+      st->done = 1;
+    }
+    st->sel = s;
+    st->moved = 1;
+  }
+}
+
+// regen = grids[sel] after a step (grid-stride copy).
+__global__ void vg_descent_regen_kernel(const vg_descent_state* st, const float* __restrict__ grids,
+                                        float* __restrict__ regen, long long n) {
+  if (!st->moved) return;
+  const float* src = grids + (long long)st->sel * n;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    regen[i] = src[i];
+}
+
 }  // namespace
+
+VG_API int vg_descent_candidates_f64(vg_descent_state* state, const double* pos, const double* grad,
+                                     const double* steps, double* cands, int32_t n_coords,
+                                     int32_t n_steps, int64_t max_iters, double tolerance,
+                                     void* stream) {
+  if (state == nullptr || pos == nullptr || grad == nullptr || steps == nullptr || cands == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates_f64: NULL pointer");
+  if (n_coords <= 0 || n_steps <= 0)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates_f64: empty problem");
+  vg_descent_cand_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      state, pos, grad, steps, cands, n_coords, n_steps, (long long)max_iters, tolerance);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_descent_candidates_f64", e);
+}
+
+VG_API int vg_descent_select_f64(vg_descent_state* state, const double* losses, const double* cands,
+                                 const float* grids, int32_t n_coords, int32_t n_steps,
+                                 int64_t n_voxels, int32_t patience, double* pos, double* best_pos,
+                                 float* regen, void* stream) {
+  if (state == nullptr || losses == nullptr || cands == nullptr || grids == nullptr ||
+      pos == nullptr || best_pos == nullptr || regen == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select_f64: NULL pointer");
+  if (n_coords <= 0 || n_steps <= 0 || n_voxels <= 0 || patience < 1)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select_f64: bad sizes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  vg_descent_select_kernel<<<1, 128, 0, st>>>(state, losses, cands, n_coords, n_steps, patience, pos,
+                                              best_pos);
+  long long blocks = (n_voxels + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  vg_descent_regen_kernel<<<(unsigned)blocks, 256, 0, st>>>(state, grids, regen, (long long)n_voxels);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_descent_select_f64", e);
+}
 
 VG_API size_t vg_mse_workspace_bytes(int64_t n_voxels, int32_t n_grids) {
   (void)n_voxels;

@@ -160,3 +160,27 @@ def test_estimator_and_cli_round_trip(tmp_path):
                          "--box", "0,0,0,12,12,12", "--output", str(tmp_path / "o.csv")]) == 0
     lines = (tmp_path / "o.csv").read_text().strip().splitlines()
     assert len(lines) == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graphs", [True, False])
+@pytest.mark.parametrize("max_iters,tol", [(5000, 1e-12), (7, 1e-30), (40, 1e-30)])
+def test_device_descent_equals_host_loop(max_iters, tol, graphs, monkeypatch):
+    """refine_coords (the loop on the device, stop flag read every few
+    iterations) takes exactly the steps of the host-driven loop: same
+    iterations, same best loss, bit-identical positions; including stops by
+    max_iters in the middle of a queued block."""
+    from paper_2211_08506_b200 import reversal as rv
+
+    monkeypatch.setattr(rv, "_USE_GRAPHS", graphs)
+    for i in range(min(3, len(REV["cases"]))):
+        rec = REV["cases"][i]
+        grid = _grid(rec["chans"], rec["pos"])
+        seeds = vg.ReversalState(np.array(rec["chans"]), np.array(rec["cand"]))
+        conf = vg.ReversalConfig(max_iters=max_iters, tolerance=tol)
+        a = rv.refine_coords(grid, seeds, conf)
+        b = rv._refine_host(grid, seeds, conf)
+        assert a.iterations == b.iterations
+        assert a.loss == b.loss
+        assert a.converged == b.converged and a.diverged == b.diverged
+        assert np.array_equal(a.positions, b.positions)
