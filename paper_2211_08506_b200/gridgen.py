@@ -28,7 +28,7 @@ from __future__ import annotations
 import math
 import time
 from dataclasses import dataclass, field
-from typing import Sequence
+from collections.abc import Sequence
 
 import numpy as np
 
@@ -286,62 +286,123 @@ def _consistency_error(points, spec: GridSpec):
     return None
 
 
+class _BoxSpecs(Sequence):
+    """Per-molecule GridSpecs of the per-molecule-bbox policy, built on access
+    (a batch of thousands of molecules should not pay for thousands of
+    validated GridSpec objects up front)."""
+
+    def __init__(self, spec: GridSpec, origin: np.ndarray, extents: np.ndarray, errors: dict):
+        self._spec, self._origin, self._extents, self._errors = spec, origin, extents, errors
+
+    def __len__(self) -> int:
+        return len(self._origin)
+
+    def __getitem__(self, b):
+        if isinstance(b, slice):
+            return [self[i] for i in range(*b.indices(len(self)))]
+        if b < 0:
+            b += len(self)
+        if b in self._errors:
+            return self._spec
+        box = BoundingBox(tuple(self._origin[b].tolist()), tuple(self._extents[b].tolist()))
+        s = self._spec
+        return GridSpec(s.shape, s.channels, box, s.sigma, s.periodic)
+
+
 def _bbox_policy(sets, spec: GridSpec, padding_sigmas: float, errors: dict):
     """Per-molecule padded boxes (gridgen.py:192-197 + core.py:283-312), in
-    fp64 with the reference's exact op order; returns (origin, delta, specs)."""
+    fp64 with the reference's exact op order, vectorised over the batch;
+    returns (origin, delta, specs)."""
     B = len(sets)
     origin = np.zeros((B, 3))
     delta = np.ones((B, 3))
-    specs = []
+    extents = np.ones((B, 3))
     H, W, D = spec.shape
     pad = padding_sigmas * float(spec.sigma)
-    for b, ps in enumerate(sets):
-        if b in errors:
-            specs.append(spec)
-            continue
-        try:
-            if len(ps) == 0:
-                raise ValueError("cannot compute a bounding box of an empty particle set")
-            if padding_sigmas < 0.0:
-                raise ValueError(f"padding_sigmas must be >= 0, got {padding_sigmas}")
-            pos = np.asarray(ps.positions, dtype=np.float64)
-            lo = pos.min(axis=0) - pad
-            hi = pos.max(axis=0) + pad
-            ext = np.maximum(hi - lo, 0.0)
-            if ext.min() <= 0.0:
-                raise ValueError("degenerate bounding box (zero extent on some axis); "
-                                 "use padding_sigmas > 0 or a positive min_extent")
-            org = 0.5 * (lo + hi) - 0.5 * ext
-            box = BoundingBox(tuple(org.tolist()), tuple(ext.tolist()))
-            mspec = GridSpec(spec.shape, spec.channels, box, spec.sigma, spec.periodic)
-        except Exception as exc:  # noqa: BLE001 - recorded per index like the reference
+    counts = np.array([len(ps) for ps in sets], dtype=np.int64)
+    live = np.array([b not in errors for b in range(B)], dtype=bool)
+    if padding_sigmas < 0.0:
+        for b in np.flatnonzero(live):
+            errors[int(b)] = ValueError(f"padding_sigmas must be >= 0, got {padding_sigmas}")
+        return origin, delta, _BoxSpecs(spec, origin, extents, errors)
+    for b in np.flatnonzero(live & (counts == 0)):
+        errors[int(b)] = ValueError("cannot compute a bounding box of an empty particle set")
+    use = np.flatnonzero(live & (counts > 0))
+    if use.size:
+        pos = np.concatenate([np.asarray(sets[b].positions, dtype=np.float64) for b in use])
+        starts = np.concatenate([[0], np.cumsum(counts[use])[:-1]])
+        lo = np.minimum.reduceat(pos, starts, axis=0) - pad
+        hi = np.maximum.reduceat(pos, starts, axis=0) + pad
+        ext = np.maximum(hi - lo, 0.0)
+        org = 0.5 * (lo + hi) - 0.5 * ext
+        bad = ext.min(axis=1) <= 0.0
+        for b in use[bad]:
+            errors[int(b)] = ValueError("degenerate bounding box (zero extent on some axis); "
+                                        "use padding_sigmas > 0 or a positive min_extent")
+        # overflowing boxes: record whatever GridSpec validation raises, as before
+        odd = ~bad & ~(np.isfinite(ext).all(axis=1) & np.isfinite(org).all(axis=1))
+        for i in np.flatnonzero(odd):
+            try:
+                GridSpec(spec.shape, spec.channels,
+                         BoundingBox(tuple(org[i].tolist()), tuple(ext[i].tolist())),
+                         spec.sigma, spec.periodic)
+            except Exception as exc:  # noqa: BLE001 - recorded per index like the reference
+                errors[int(use[i])] = exc
+                bad[i] = True
+        ok = use[~bad]
+        origin[ok] = org[~bad]
+        extents[ok] = ext[~bad]
+        delta[ok] = ext[~bad] / np.array([W, H, D], dtype=np.float64)
+    return origin, delta, _BoxSpecs(spec, origin, extents, errors)
+
+
+def _batch_errors(sets: Sequence, spec: GridSpec) -> dict:
+    """Per-index consistency errors (gridgen.py:114-127): vectorised channel
+    check; per-molecule checks only where periodicity is involved or a
+    molecule fails (for the reference's exact message)."""
+    errors: dict = {}
+    C = spec.channels
+    periodic = spec.periodic is not None
+    suspects = [b for b, ps in enumerate(sets)
+                if periodic or getattr(ps, "lattice", None) is not None]
+    if sets:
+        maxch = _max_channels(sets)
+        suspects = sorted(set(suspects) | set(np.flatnonzero(maxch >= C).tolist()))
+    for b in suspects:
+        exc = _consistency_error(sets[b], spec)
+        if exc is not None:
             errors[b] = exc
-            specs.append(spec)
-            continue
-        origin[b] = box.origin
-        delta[b] = (box.extents[0] / W, box.extents[1] / H, box.extents[2] / D)
-        specs.append(mspec)
-    return origin, delta, specs
+    return errors
+
+
+def _max_channels(sets: Sequence) -> np.ndarray:
+    counts = np.array([len(ps) for ps in sets], dtype=np.int64)
+    out = np.full(len(sets), -1, dtype=np.int64)
+    nz = np.flatnonzero(counts)
+    if nz.size:
+        ch = np.concatenate([sets[b].channels for b in nz])
+        starts = np.concatenate([[0], np.cumsum(counts[nz])[:-1]])
+        out[nz] = np.maximum.reduceat(ch, starts)
+    return out
 
 
 def pack_particle_sets(sets: Sequence, spec: GridSpec, errors: dict):
     """CSR arrays of every molecule without a recorded error (failed molecules
     get an empty atom range, hence an all-zero grid slot)."""
     B = len(sets)
-    counts = np.zeros(B, dtype=np.int64)
-    for b, ps in enumerate(sets):
-        if b not in errors:
-            counts[b] = len(ps)
+    counts = np.array([len(ps) for ps in sets], dtype=np.int64).reshape(B)
+    for b in errors:
+        counts[b] = 0
     offsets = np.zeros(B + 1, dtype=np.int64)
     np.cumsum(counts, out=offsets[1:])
-    n = int(offsets[-1])
-    channels = np.empty(n, dtype=np.int32)
-    xyz = np.empty((n, 3), dtype=np.float64)
-    for b, ps in enumerate(sets):
-        if counts[b]:
-            lo, hi = offsets[b], offsets[b + 1]
-            channels[lo:hi] = ps.channels
-            xyz[lo:hi] = ps.positions
+    keep = np.flatnonzero(counts)
+    if keep.size:
+        channels = np.concatenate([sets[b].channels for b in keep]).astype(np.int32)
+        xyz = np.concatenate([np.asarray(sets[b].positions, dtype=np.float64).reshape(-1, 3)
+                              for b in keep])
+    else:
+        channels = np.empty(0, dtype=np.int32)
+        xyz = np.empty((0, 3), dtype=np.float64)
     return offsets, channels, xyz, counts
 
 
@@ -362,11 +423,7 @@ def generate_batch(point_sets: Sequence, spec: GridSpec, spec_policy: str = "fix
     _check_mode(mode)
     _check_dtype(dtype)
     start = time.perf_counter()
-    errors: dict = {}
-    for b, ps in enumerate(point_sets):
-        exc = _consistency_error(ps, spec)
-        if exc is not None:
-            errors[b] = exc
+    errors = _batch_errors(point_sets, spec)
     mol_origin = mol_delta = None
     specs = [spec] * len(point_sets)
     if spec_policy == "per-molecule-bbox":

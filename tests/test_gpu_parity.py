@@ -577,3 +577,24 @@ def test_fused_cta_fallback_on_large_molecules_vs_oracle(monkeypatch):
     assert_bitwise(grids.cpu().numpy(), ref, "fused halving")
     assert [int(v) for v in st[:, 0].cpu()] == [r["voxel_writes"] for r in rs]
     assert [int(v) for v in st[:, 1].cpu()] == [r["nonzero_voxels"] for r in rs]
+
+
+def test_estimator_packed_fast_path_equals_per_sample_path():
+    """transform's batch-at-once validation and packing (fixed box) gives the
+    per-sample path's bits, empty samples included; a sample with an
+    out-of-range channel still raises the reference's ValueError."""
+    rng = np.random.default_rng(77)
+    X = []
+    for i in range(40):
+        n = int(rng.integers(0, 12))
+        X.append(np.column_stack([rng.integers(0, 3, n), rng.uniform(0, 6, (n, 3))]))
+    X[7] = np.zeros((0, 4))
+    est = vg.GaussianVoxelizer(grid_size=(20, 18, 24), sigma=0.45, n_channels=3,
+                               box=((0.0, 0.0, 0.0), (6.0, 6.0, 6.0))).fit(X)
+    fast = est.transform(X)
+    slow = vg.generate_batch(est._sets(X), est._spec()).tensor
+    assert np.array_equal(fast.cpu().numpy().view(np.uint32), slow.cpu().numpy().view(np.uint32))
+    bad = list(X)
+    bad[3] = np.array([[5.0, 1.0, 1.0, 1.0]])
+    with pytest.raises(ValueError):
+        est.transform(bad)

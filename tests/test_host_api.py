@@ -225,3 +225,47 @@ def test_synth_configs_follow_baseline():
             assert d[np.triu_indices(len(xyz), 1)].min() >= cfg.min_dist
     pb = synth.packed_batch(c3, [0])
     assert 1500 <= pb.n_molecules * 0 + len(pb.channels) <= 3000
+
+
+def test_vectorised_batch_host_path_matches_per_molecule_semantics():
+    """generate_batch's vectorised validation, packing and per-molecule boxes
+    give the per-molecule results (reference gridgen.py:114-127, 173-221,
+    core.py:283-312) on a mixed batch: bad channels, empty sets, a single
+    atom, huge coordinates."""
+    rng = np.random.default_rng(11)
+    spec = vg.GridSpec((10, 12, 14), 3, vg.BoundingBox((0, 0, 0), (5, 5, 5)), 0.4)
+    sets = []
+    for b in range(200):
+        n = int(rng.integers(0, 9))
+        ch = rng.integers(0, 3, n)
+        if b % 37 == 5 and n:
+            ch[0] = 7            # out-of-range channel
+        sets.append(vg.ParticleSet(ch, rng.normal(2.5, 3.0, (n, 3))))
+    sets.append(vg.ParticleSet([0], [[1e300, -1e300, 0.0]]))
+    errors = gridgen._batch_errors(sets, spec)
+    slow = {b: e for b, ps in enumerate(sets)
+            if (e := gridgen._consistency_error(ps, spec)) is not None}
+    assert sorted(errors) == sorted(slow)
+    assert all(str(errors[b]) == str(slow[b]) for b in slow)
+    offsets, ch, xyz, counts = gridgen.pack_particle_sets(sets, spec, errors)
+    for b, ps in enumerate(sets):
+        lo, hi = offsets[b], offsets[b + 1]
+        if b in errors:
+            assert hi == lo
+        else:
+            assert np.array_equal(ch[lo:hi], ps.channels) and np.array_equal(xyz[lo:hi], ps.positions)
+    errs2 = dict(errors)
+    origin, delta, specs = gridgen._bbox_policy(sets, spec, 4.0, errs2)
+    assert len(specs) == len(sets)
+    for b, ps in enumerate(sets):
+        if b in errors:
+            continue
+        try:
+            box = vg.bounding_box_of(ps, 0.4, 4.0)
+        except ValueError:
+            assert b in errs2
+            continue
+        assert b not in errs2
+        assert specs[b].box == box
+        assert tuple(origin[b]) == box.origin
+        assert tuple(delta[b]) == (box.extents[0] / 12, box.extents[1] / 10, box.extents[2] / 14)
