@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -88,6 +89,18 @@ constexpr int kBinWarps = 32;                 // K2: warps per molecule CTA
 constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Function attributes (dynamic shared memory limit, carveout) are set per
+// device: true the first time a kernel instance is launched on the current
+// device by any thread (setting them twice is harmless).
+bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return false;
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return true;
+}
 int round_up4(int v) { return (v + 3) & ~3; }
 
 // Tuning / test hooks (VG_* environment variables, read at launch time so
@@ -1183,7 +1196,7 @@ __device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* 
 
 #ifdef VG_EXP_TIMING
 // Experiment builds only (-DVG_EXP_TIMING): per-CTA phase timestamps.
-__device__ unsigned long long g_vg_ts[1 << 17][8];
+__device__ unsigned long long g_vg_ts[1 << 17][12];
 __device__ __forceinline__ unsigned long long vg_gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1340,6 +1353,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
       const AtomFilter f{c, js, je, T.row_base, T.row_end, T.zv0, T.zv1};
       int64_t pos = src_begin;
       int n = build_list(p.supp, sh, src, pos, src_end, f);
+      if (rounds == 0) VG_TS(8);
       if ((pos < src_end || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
         sc = (sc + 1) >> 1;
         continue;
@@ -1356,6 +1370,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
           stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
           Counts<M> cnt;
           build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, T.row_base, rlo0, rhi0, R, cnt);
+          if (rounds == 0) VG_TS(9);
           cp_async_wait_all();
           __syncthreads();  // staged tables visible to every warp (lists are warp-private)
           if (rounds == 0) VG_TS(2);
@@ -1695,13 +1710,12 @@ template <int M, int SW, int YP>
 void launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   // The row kernel is register-limited to 4 CTAs/SM; ask for the largest
   // shared-memory carveout so that shared memory never lowers that.
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};
+  if (first_on_device(configured)) {
     cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          96 * 1024);
-    configured = true;
   }
   vg_slab_kernel<M, SW, YP><<<grid, nt, smem, st>>>(p);
 }
@@ -1724,9 +1738,9 @@ void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const S
 // shared-memory budget keeps as many CTAs resident as the registers allow.
 template <int SW, int YP>
 int rows_regs_sw(int M) {
-  static int regs[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  static std::atomic<int> regs[9];   // zero-initialised (static storage)
   const int m = M < 1 ? 1 : (M > 8 ? 8 : M);
-  if (regs[m] == 0) {
+  if (regs[m].load(std::memory_order_relaxed) == 0) {
     cudaFuncAttributes a;
     cudaError_t e = cudaErrorInvalidValue;
     switch (m) {
@@ -1939,11 +1953,10 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     bp.nch = p.n_jchunks;
     bp.jc = jc;
     const size_t bsmem = (size_t)(kBinWarps + 1) * nb * sizeof(int);
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    if (first_on_device(configured)) {
       cudaFuncSetAttribute(vg_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (kBinWarps + 1) * kMaxBins * (int)sizeof(int));
-      configured = true;
     }
     vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
     if (kernels != nullptr) *kernels += 1;

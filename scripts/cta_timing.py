@@ -19,7 +19,7 @@ xyz = torch.as_tensor(pb.xyz).cuda()
 for _ in range(4):
     g, st = vg.generate_packed(off, ch, xyz, spec)
 torch.cuda.synchronize()
-buf = np.zeros((1 << 17, 8), np.uint64)
+buf = np.zeros((1 << 17, 12), np.uint64)
 lib = _native.lib()
 fn = lib.vg_exp_timing_fetch
 fn.restype = ctypes.c_int

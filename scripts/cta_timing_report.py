@@ -9,7 +9,8 @@ sm=a[:,5]>>32; c=a[:,5]&0xffffffff; rounds=a[:,6]>>32; staged=a[:,6]&0xffffffff
 dur=t4-t0
 print('kernel span us', (t4.max())/1e3, 'CTAs', n)
 print('CTA dur us: mean %.2f med %.2f p90 %.2f max %.2f'%(dur.mean()/1e3, np.median(dur)/1e3, np.percentile(dur,90)/1e3, dur.max()/1e3))
-ph=[('start->l0',t1-t0),('l0->staged',t2-t1),('staged->lastacc',t3-t2),('lastacc->end',t4-t3)]
+t8=a[:,8]-base; t9=a[:,9]-base
+ph=[('start->l0',t1-t0),('l0->list',t8-t1),('list->issued',t9-t8),('issued->staged',t2-t9),('staged->lastacc',t3-t2),('lastacc->end',t4-t3)]
 for k,v in ph: print('  %-16s mean %.2f us'%(k, v.mean()/1e3))
 # per channel
 for ch in np.unique(c):
