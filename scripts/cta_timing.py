@@ -26,4 +26,10 @@ fn.restype = ctypes.c_int
 fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert fn(buf.ctypes.data, buf.nbytes) == 0
 np.save(sys.argv[2], buf)
+wbuf = np.zeros((1 << 17, 8), np.uint64)
+fw = lib.vg_exp_timing_fetch_warps
+fw.restype = ctypes.c_int
+fw.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+assert fw(wbuf.ctypes.data, wbuf.nbytes) == 0
+np.save(sys.argv[2].replace(".npy", "_warps.npy"), wbuf)
 print("saved", sys.argv[2])
