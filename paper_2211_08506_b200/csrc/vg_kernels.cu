@@ -1197,6 +1197,7 @@ __device__ __forceinline__ void build_sublists(const SlabParams& p, const int4* 
 #ifdef VG_EXP_TIMING
 // Experiment builds only (-DVG_EXP_TIMING): per-CTA phase timestamps.
 __device__ unsigned long long g_vg_ts[1 << 17][12];
+__device__ unsigned long long g_vg_ts_w[1 << 17][8];   // per-warp hot-loop end
 __device__ __forceinline__ unsigned long long vg_gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1386,6 +1387,10 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
                                                  R * p.D, je - js, ibase, T.row_end, R, cnt,
                                                  lists_s, p.stage_cap, gx_off, gz_off, half);
           VG_TS(3);
+#ifdef VG_EXP_TIMING
+          // per-warp end of the hot loop (lane 0 of each warp)
+          if ((tid & 31) == 0 && blockIdx.x < (1u << 17)) g_vg_ts_w[blockIdx.x][warp] = vg_gtime();
+#endif
           __syncthreads();  // the next segment / sub-chunk rewrites the staging area
           first = false;
         }
@@ -2171,6 +2176,11 @@ VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
 }
 
 #ifdef VG_EXP_TIMING
+VG_API int vg_exp_timing_fetch_warps(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_vg_ts_w, bytes < sizeof(g_vg_ts_w) ? bytes : sizeof(g_vg_ts_w)) ==
+                 cudaSuccess ? VG_OK : VG_ERR_CUDA;
+}
+
 VG_API int vg_exp_timing_fetch(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_vg_ts, bytes < sizeof(g_vg_ts) ? bytes : sizeof(g_vg_ts)) ==
                  cudaSuccess ? VG_OK : VG_ERR_CUDA;
