@@ -147,7 +147,7 @@ class GridPipeline:
 
         desc = slot.desc
         if desc is None:
-            desc = slot.desc = self.engine.describe(off_d, ch_d, xyz_d.view(-1, 3), spec,
+            desc = slot.desc = self.engine.describe(off_d, ch_d, xyz_d, spec,
                                                     mode=self.mode, threshold=self.threshold)
         desc.n_molecules = B
         desc.n_atoms = n

@@ -598,3 +598,33 @@ def test_estimator_packed_fast_path_equals_per_sample_path():
     bad[3] = np.array([[5.0, 1.0, 1.0, 1.0]])
     with pytest.raises(ValueError):
         est.transform(bad)
+
+
+def test_pipeline_edge_batches():
+    """GridPipeline over an empty batch, a batch of empty molecules and a
+    periodic spec, reusing slots: every result equals the serial path and the
+    library reports the kernels it launched."""
+    from paper_2211_08506_b200.loader import GridPipeline
+
+    cfg = synth.CONFIGS[0]
+    spec = spec_of(cfg)
+    pipe = GridPipeline(spec, depth=2)
+    r0 = pipe.submit(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros((0, 3)))
+    r0.ready.synchronize()
+    assert tuple(r0.grids.shape) == (0, 5, 32, 32, 32) and pipe.launches == 0
+    r1 = pipe.submit(np.zeros(4, np.int64), np.zeros(0, np.int32), np.zeros((0, 3)))
+    r1.ready.synchronize()
+    assert not r1.grids.any() and pipe.launches == 1          # K3 only (no atoms: no K1)
+    pb = synth.packed_batch(cfg, range(5))
+    r2 = pipe.submit(pb.offsets, pb.channels, pb.xyz)
+    r2.ready.synchronize()
+    g_ref, _ = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+    assert_bitwise(r2.grids.cpu().numpy(), g_ref.cpu().numpy(), "pipeline after empty")
+    assert pipe.launches == 3
+    cell = vg.LatticeCell((10.0, 10.0, 10.0))
+    pspec = vg.GridSpec((32, 32, 32), 5, vg.BoundingBox((0, 0, 0), (10, 10, 10)), 0.5, cell)
+    ppipe = GridPipeline(pspec)
+    r3 = ppipe.submit(pb.offsets, pb.channels, np.mod(pb.xyz, 10.0))
+    r3.ready.synchronize()
+    g_per, _ = vg.generate_packed(pb.offsets, pb.channels, np.mod(pb.xyz, 10.0), pspec)
+    assert_bitwise(r3.grids.cpu().numpy(), g_per.cpu().numpy(), "pipeline periodic")
