@@ -163,3 +163,19 @@ def test_submit_validates_before_touching_the_gpu(lib):
     layout = _native.VgWsLayout()
     assert lib.vg_workspace_layout(d, layout) == 0
     assert need.value == layout.total > 0
+
+
+def test_descent_entry_points_validate_arguments(lib):
+    """The device-descent calls reject NULL buffers and empty sizes before any
+    launch (no GPU needed)."""
+    assert lib.vg_descent_candidates_f64(None, 8, 8, 8, 8, 3, 11, 10, 1e-12, None) == -1
+    assert lib.vg_descent_candidates_f64(8, 8, 8, 8, 8, 0, 11, 10, 1e-12, None) == -1
+    assert lib.vg_descent_select_f64(8, 8, 8, 8, 3, 11, 100, 0, 8, 8, 8, None) == -1
+    assert lib.vg_descent_select_f64(8, None, 8, 8, 3, 11, 100, 10, 8, 8, 8, None) == -1
+    assert _native.VgDescentState.__dict__ and ctypes_sizeof_state() == 48
+
+
+def ctypes_sizeof_state():
+    import ctypes
+
+    return ctypes.sizeof(_native.VgDescentState)
