@@ -283,7 +283,10 @@ def run_b200(args):
     if args.scaling == "weak":
         indices = range(rank * B, (rank + 1) * B)       # distinct molecules per rank
     else:
-        indices = shard.shard_range(B, rank, world)       # fixed total, split by rank
+        # fixed total, split by rank into cost-balanced contiguous ranges
+        costs = shard.molecule_costs(synth.atom_counts(cfg, range(B)), cfg.grid_bytes,
+                                     shard.BYTES_PER_ATOM)
+        indices = shard.shard_range(B, rank, world, costs)
     t0 = time.perf_counter()
     pb = synth.packed_batch(cfg, indices)
     log(f"[bench rank{rank}] synthesized {pb.n_molecules} molecules / {len(pb.channels)} atoms "

@@ -11,7 +11,13 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["molecule_costs", "plan_shards", "shard_range"]
+__all__ = ["BYTES_PER_ATOM", "molecule_costs", "plan_shards", "shard_range"]
+
+
+# K3 cost of one atom in output-byte equivalents, from per-CTA timing of
+# cfg4 on a B200 (5-20 atom molecules: 174 CTA-us for 2.2 MB of grid;
+# 150-200 atoms: 461 CTA-us): ~1.76 us per atom ~ 22 KB of writes.
+BYTES_PER_ATOM = 22_000.0
 
 
 def molecule_costs(atom_counts, grid_bytes: int, bytes_per_atom: float = 0.0) -> np.ndarray:

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["SynthConfig", "CONFIGS", "molecule", "packed_batch", "PackedBatch"]
+__all__ = ["SynthConfig", "CONFIGS", "atom_counts", "molecule", "packed_batch", "PackedBatch"]
 
 _SMALL_P = (0.5, 0.35, 0.07, 0.07, 0.01)                     # H C N O F
 # BASELINE lists (H,C,N,O,S,P,Fe,Zn) p=(.49,.31,.08,.09,.01,.005,.0025,.0025),
@@ -83,6 +83,14 @@ def _draw(cfg: SynthConfig, rng, m: int) -> np.ndarray:
     if kind == "uniform":
         return rng.uniform(a, b, size=(m, 3))
     return rng.normal(a, b, size=(m, 3))
+
+
+def atom_counts(cfg: SynthConfig, indices) -> np.ndarray:
+    """Atom count of each molecule in ``indices`` without drawing its atoms
+    (the count is the first draw of the molecule's generator), for
+    cost-balanced sharding."""
+    return np.array([_atom_count(cfg, np.random.default_rng([cfg.seed, int(i)]))
+                     for i in indices], dtype=np.int64)
 
 
 def molecule(cfg: SynthConfig, index: int):

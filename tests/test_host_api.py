@@ -269,3 +269,21 @@ def test_vectorised_batch_host_path_matches_per_molecule_semantics():
         assert specs[b].box == box
         assert tuple(origin[b]) == box.origin
         assert tuple(delta[b]) == (box.extents[0] / 12, box.extents[1] / 10, box.extents[2] / 14)
+
+
+def test_atom_counts_match_generated_molecules_and_cost_shards():
+    from paper_2211_08506_b200 import shard, synth
+
+    for k in (0, 4):
+        cfg = synth.CONFIGS[k]
+        idx = range(10, 30)
+        pb = synth.packed_batch(cfg, idx)
+        assert np.array_equal(synth.atom_counts(cfg, idx), np.diff(pb.offsets))
+    cfg = synth.CONFIGS[4]
+    costs = shard.molecule_costs(synth.atom_counts(cfg, range(512)), cfg.grid_bytes,
+                                 shard.BYTES_PER_ATOM)
+    plan = shard.plan_shards(costs, 8)
+    assert plan[0][0] == 0 and plan[-1][1] == 512
+    assert all(a[1] == b[0] for a, b in zip(plan, plan[1:]))
+    per = [costs[a:b].sum() for a, b in plan]
+    assert max(per) / min(per) < 1.05
