@@ -631,35 +631,37 @@ __device__ __forceinline__ void store_slot(float* slab, int f, const float4& v) 
 }
 __device__ __forceinline__ void store_slot(float* slab, int f, const float& v) { __stcs(slab + f, v); }
 
-__device__ long long block_sum(SlabShared& sh, long long v) {
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh.red[warp] = v;
-  __syncthreads();
-  long long t = 0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < nw; ++w) t += sh.red[w];
-  return t;  // valid in thread 0
-}
 
 // Per-molecule counters: nonzero voxels of this CTA (integer atomics are
 // order-independent) and, from one CTA per molecule, voxel_writes.
+// Per-molecule counters, warp by warp: integer atomics are order-independent,
+// so no block reduction (and no barrier) is needed at the end of a CTA.
+// nonzero_voxels sums every CTA's count; voxel_writes (gridgen.py:103, the
+// sum of support-box volumes) comes from one CTA per molecule. Both start
+// from the zeros launch_slabs writes.
+__device__ __forceinline__ long long warp_sum(long long v) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+  return v;  // lane 0
+}
+
 __device__ void finish_stats(const SlabParams& p, SlabShared& sh, int64_t b, int64_t a0,
                              int64_t a1, long long nz, bool owner) {
-  const long long tot = block_sum(sh, nz);
-  if (threadIdx.x == 0 && tot != 0)
+  (void)sh;
+  const bool lane0 = (threadIdx.x & 31) == 0;
+  const long long tot = warp_sum(nz);
+  if (lane0 && tot != 0)
     atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[b].nonzero_voxels),
               (unsigned long long)tot);
   if (owner) {
-    // voxel_writes = sum of support-box volumes (gridgen.py:103)
     long long w = 0;
     for (int64_t a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
       const int4 s = __ldg(p.supp + a);
       w += (long long)(hi16(s.x) - lo16(s.x)) * (hi16(s.y) - lo16(s.y)) * (hi16(s.z) - lo16(s.z));
     }
-    const long long wt = block_sum(sh, w);
-    if (threadIdx.x == 0) p.stats[b].voxel_writes = wt;
+    const long long wt = warp_sum(w);
+    if (lane0 && wt != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[b].voxel_writes),
+                (unsigned long long)wt);
   }
 }
 
@@ -1067,8 +1069,10 @@ __device__ __noinline__ int accumulate_rows_pair(float* base, int64_t slab_elems
       }
       // counted only where some candidate was active (a vote: a real branch,
       // not a predicated count, on the many untouched pairs)
+#ifndef VG_EXP_NOCOUNT
       if (__any_sync(kFull, touched) && mine)
         nz += nonzeros_pos(acc0) + (pair ? nonzeros_pos(acc1) : 0) - before;
+#endif
     }
   }
   return nz;
