@@ -98,8 +98,8 @@ int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
  * GaussianVoxelizer.transform, estimator.py:134-151, minus the np.stack):
  * copy_stream  waits ev_wait, H2D of the host CSR arrays (when h_* != NULL)
  *              into desc->offsets/channel/xyz, records ev_copied;
- * tables_stream waits ev_wait + ev_copied, K1, records ev_tabled;
- * compute_stream waits ev_wait + ev_tabled, K2/K3, then the D2H of the
+ * tables_stream waits ev_copied (hence ev_wait), K1, records ev_tabled;
+ * compute_stream waits ev_tabled (hence ev_wait), K2/K3, then the D2H of the
  *              per-grid stats into h_stats (when != NULL), records ev_done.
  * Events are caller-created cudaEvent_t (passed as void*); ev_wait may be
  * NULL and may be the same event as ev_done (the wait uses its previous

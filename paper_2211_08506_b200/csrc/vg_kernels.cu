@@ -32,6 +32,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <unistd.h>   // environ
+
 #include "../../include/voxgrid_b200.h"
 #include "vg_math.cuh"
 
@@ -103,11 +105,40 @@ bool first_on_device(std::atomic<unsigned long long>& mask) {
 }
 int round_up4(int v) { return (v + 3) & ~3; }
 
-// Tuning / test hooks (VG_* environment variables, read at launch time so
-// that tests can switch code paths inside one process): the integer value of
-// `name` if it is set, parses fully and lies in [lo, hi]; otherwise dflt.
+// Tuning / test hooks (VG_* environment variables, read at every API call so
+// that tests can switch code paths inside one process). One scan of environ
+// per call copies the VG_* entries (a launch consults ~20 hooks; 20 getenv
+// scans cost several microseconds of host time per batch).
+constexpr int kEnvMax = 32, kEnvLen = 64;
+struct EnvSnap {
+  int n = 0;
+  char kv[kEnvMax][kEnvLen];
+};
+thread_local EnvSnap g_env;
+
+void refresh_env() {
+  g_env.n = 0;
+  for (char** e = environ; e != nullptr && *e != nullptr; ++e) {
+    const char* v = *e;
+    if (v[0] == 'V' && v[1] == 'G' && v[2] == '_' && g_env.n < kEnvMax) {
+      strncpy(g_env.kv[g_env.n], v, kEnvLen - 1);
+      g_env.kv[g_env.n][kEnvLen - 1] = '\0';
+      ++g_env.n;
+    }
+  }
+}
+
+const char* env_get(const char* name) {
+  const size_t len = strlen(name);
+  for (int i = 0; i < g_env.n; ++i)
+    if (strncmp(g_env.kv[i], name, len) == 0 && g_env.kv[i][len] == '=') return g_env.kv[i] + len + 1;
+  return nullptr;
+}
+
+// The integer value of hook `name` if it is set, parses fully and lies in
+// [lo, hi]; otherwise dflt.
 int env_int(const char* name, int dflt, int lo, int hi) {
-  const char* v = getenv(name);
+  const char* v = env_get(name);
   if (v == nullptr || *v == '\0') return dflt;
   char* end = nullptr;
   const long x = strtol(v, &end, 10);
@@ -1539,6 +1570,7 @@ __global__ void vg_fill_tail_kernel(float* __restrict__ out, int64_t n, float v)
 // host-side validation + launch planning
 // ---------------------------------------------------------------------------
 int validate(const vg_batch_desc* d) {
+  refresh_env();   // every planning entry point validates first
   if (d == nullptr) return set_error(VG_ERR_INVALID, "descriptor is NULL");
   if (d->n_molecules < 0 || d->n_atoms < 0)
     return set_error(VG_ERR_INVALID, "negative molecule or atom count");
@@ -2108,12 +2140,10 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
     if (e == cudaSuccess) e = r;
     return e == cudaSuccess;
   };
-  // slot reuse: every stage waits for the slot's previous consumer
-  if (ev_wait != nullptr) {
-    ok(cudaStreamWaitEvent(cs, ev_wait, 0));
-    ok(cudaStreamWaitEvent(ts, ev_wait, 0));
-    ok(cudaStreamWaitEvent(ks, ev_wait, 0));
-  }
+  // slot reuse: the copy stage waits for the slot's previous consumer; K1
+  // and K3 follow it through ev_copied / ev_tabled, so they are ordered
+  // after that consumer too
+  if (ev_wait != nullptr) ok(cudaStreamWaitEvent(cs, ev_wait, 0));
   if (a->h_offsets != nullptr && B > 0)
     ok(cudaMemcpyAsync(const_cast<int64_t*>(desc->offsets), a->h_offsets, (size_t)(B + 1) * 8,
                        cudaMemcpyHostToDevice, cs));

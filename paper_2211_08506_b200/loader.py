@@ -55,6 +55,8 @@ class _Slot:
         self.kernels = ctypes.c_int32(0)           # kernels the last submit launched
         self.used = False
         self._host = None
+        self.out_b = -1                           # batch size `out` was allocated for
+        self.ptrs = None                          # (out, ws, ws bytes, stats) pointers
 
 
 class GridPipeline:
@@ -90,6 +92,12 @@ class GridPipeline:
             t = torch.empty(max(need, 1), dtype=dtype, device=self.device)
         return t
 
+    def _dev(self, t, dtype):
+        # a contiguous device tensor of `dtype` (the input itself when it is one)
+        if t.dtype is dtype and t.device == self.device and t.is_contiguous():
+            return t
+        return t.to(self.device, dtype).contiguous()
+
     def submit(self, offsets, channels, xyz, release=None, stats_out=None) -> PipelineResult:
         """Queue one CSR batch (numpy/torch, host or device). Returns at once.
 
@@ -102,8 +110,8 @@ class GridPipeline:
         spec = self.spec
         slot = self.slots[self.k % len(self.slots)]
         self.k += 1
-        B = int(len(offsets) - 1)
-        n = int(len(channels))
+        B = int(offsets.shape[0]) - 1
+        n = int(channels.shape[0])
         H, W, D = spec.shape
         if release is not None:
             for st in (self.copy_stream, self.tables_stream, self.compute_stream):
@@ -126,12 +134,13 @@ class GridPipeline:
         # buffers are rewritten (no wait on the slot's first use)
         args.ev_wait = slot.events[2].cuda_event if slot.used else None
         slot.used = True
-        if all(isinstance(t, torch.Tensor) and t.is_cuda for t in (offsets, channels, xyz)):
+        if (isinstance(offsets, torch.Tensor) and offsets.is_cuda and isinstance(channels, torch.Tensor)
+                and channels.is_cuda and isinstance(xyz, torch.Tensor) and xyz.is_cuda):
             # device-resident inputs: used in place when they already have the
             # kernel's dtypes (caller keeps them unchanged until `ready`)
-            off_d = offsets.to(self.device, torch.int64).contiguous()
-            ch_d = channels.to(self.device, torch.int32).contiguous()
-            xyz_d = xyz.to(self.device, torch.float64).contiguous().reshape(-1)
+            off_d = self._dev(offsets, torch.int64)
+            ch_d = self._dev(channels, torch.int32)
+            xyz_d = self._dev(xyz, torch.float64)
             args.h_offsets = args.h_channel = args.h_xyz = None
             host = (off_d, ch_d, xyz_d)
         else:
@@ -154,19 +163,25 @@ class GridPipeline:
         desc.offsets = off_d.data_ptr()
         desc.channel = ch_d.data_ptr() if n else None
         desc.xyz = xyz_d.data_ptr() if n else None
-        shape = (B, spec.channels, H, W, D)
-        if slot.out is None or tuple(slot.out.shape) != shape:
-            slot.out = torch.empty(shape, dtype=torch.float32, device=self.device)
+        if slot.out_b != B:
+            slot.out = torch.empty((B, spec.channels, H, W, D), dtype=torch.float32,
+                                   device=self.device)
             slot.stats = torch.empty((B, 2), dtype=torch.int64, device=self.device)
+            slot.out_b = B
+            slot.ptrs = None
         args.h_stats = stats_out.data_ptr() if stats_out is not None else None
         if slot.ws is None:
             slot.ws = torch.empty(1 << 20, dtype=torch.uint8, device=self.device)
-        rc = self.lib.vg_submit_f32(desc, args, slot.out.data_ptr(), slot.ws.data_ptr(),
-                                    slot.ws.numel(), slot.stats.data_ptr())
+            slot.ptrs = None
+        if slot.ptrs is None:
+            slot.ptrs = (slot.out.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
+                         slot.stats.data_ptr())
+        rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         if rc == _native.VG_ERR_WORKSPACE and slot.ws_needed.value > slot.ws.numel():
             slot.ws = torch.empty(slot.ws_needed.value, dtype=torch.uint8, device=self.device)
-            rc = self.lib.vg_submit_f32(desc, args, slot.out.data_ptr(), slot.ws.data_ptr(),
-                                        slot.ws.numel(), slot.stats.data_ptr())
+            slot.ptrs = (slot.out.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
+                         slot.stats.data_ptr())
+            rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         _native.check(rc, "vg_submit_f32")
         self.launches += slot.kernels.value   # K1, K2 (binned batches), K3
         # keep the inputs alive until the copy / kernels have read them
@@ -188,6 +203,8 @@ def _host_array(a, dtype):
     import torch
 
     if isinstance(a, torch.Tensor):
+        if a.dtype is dtype and not a.is_cuda and a.is_contiguous():
+            return a          # e.g. pinned_csr() tensors: used in place
         t = a.cpu()
     else:
         t = torch.from_numpy(np.asarray(a))
