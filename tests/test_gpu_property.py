@@ -1,4 +1,4 @@
-"""Randomised parity (hypothesis): random shapes, channel counts, boxes,
+"""Randomised parity (hypothesis, 1000 + 300 derandomised cases): random shapes, channel counts, boxes,
 sigmas, thresholds, periodic cells and molecule sizes, GPU path vs the CPU
 oracle, bit for bit, with identical GenStats counters. Complements the fixed
 cases of test_gpu_parity.py with inputs nobody chose by hand."""
@@ -38,7 +38,7 @@ def batches(draw):
     return H, W, D, C, ext, origin, periodic, sigma, thr, sizes, seed
 
 
-@settings(max_examples=200, deadline=None, derandomize=True,
+@settings(max_examples=1000, deadline=None, derandomize=True,
           suppress_health_check=[HealthCheck.too_slow])
 @given(batches())
 def test_random_batches_match_oracle(case):
@@ -63,3 +63,31 @@ def test_random_batches_match_oracle(case):
     st_h = st_.cpu().numpy()
     assert [int(v) for v in st_h[:, 0]] == [r["voxel_writes"] for r in rs]
     assert [int(v) for v in st_h[:, 1]] == [r["nonzero_voxels"] for r in rs]
+
+
+@settings(max_examples=300, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(1, 36), st.integers(1, 36), st.integers(1, 36), st.integers(1, 4),
+       st.floats(0.1, 0.9), st.floats(0.0, 6.0),
+       st.lists(st.integers(0, 30), min_size=1, max_size=5), st.integers(0, 2**31 - 1))
+def test_random_per_molecule_boxes_match_oracle(H, W, D, C, sigma, pad, sizes, seed):
+    """spec_policy="per-molecule-bbox" (per-molecule origin and voxel size on
+    the device) against the oracle's grids in each molecule's own box."""
+    rng = np.random.default_rng(seed)
+    sets = [vg.ParticleSet(rng.integers(0, C, n), rng.normal(0.0, 3.0, (n, 3))) for n in sizes]
+    spec = vg.GridSpec((H, W, D), C, vg.BoundingBox((0, 0, 0), (1, 1, 1)), sigma)
+    res = vg.generate_batch(sets, spec, spec_policy="per-molecule-bbox", padding_sigmas=pad)
+    got = res.tensor.cpu().numpy()
+    for b, ps in enumerate(sets):
+        try:
+            origin, ext = orc.bbox_of(np.asarray(ps.positions), sigma, pad)
+        except ValueError:
+            assert b in res.errors
+            assert not got[b].any()
+            continue
+        assert b not in res.errors
+        ref, rs = orc.grid(np.asarray(ps.channels), np.asarray(ps.positions),
+                           orc.Geometry((H, W, D), C, origin, ext, sigma))
+        assert_bitwise(got[b], ref, f"bbox case {b}")
+        g, gs = res.results[b]
+        assert gs.voxel_writes == rs["voxel_writes"] and gs.nonzero_voxels == rs["nonzero_voxels"]
