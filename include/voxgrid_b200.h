@@ -141,11 +141,17 @@ int vg_erf_f32(const float* t, float* out, int64_t n, void* stream);
 size_t vg_mse_workspace_bytes(int64_t n_voxels, int32_t n_grids);
 int vg_mse_f64(const float* ref, const float* grids, int64_t n_voxels, int32_t n_grids,
                double* out, void* workspace, size_t workspace_bytes, void* stream);
+/* The same for several references: grid g is compared with refs[g / grids_per_ref]
+ * (refs: consecutive grids of n_voxels floats) — batched reversal. */
+int vg_mse_grouped_f64(const float* refs, const float* grids, int64_t n_voxels, int32_t n_grids,
+                       int32_t grids_per_ref, double* out, void* workspace,
+                       size_t workspace_bytes, void* stream);
 
 /* Replaces _gradient_from_diff / loss_gradient (reversal.py:271-318): grad
  * [n_atoms*3] (x, y, z per atom, fp64) of mean((regen - ref)^2) w.r.t. the
- * atom coordinates of ONE molecule described by desc (open boundaries;
- * regen = the grid generated from desc, ref the target, both (C,H,W,D)). */
+ * atom coordinates of the molecules described by desc (open boundaries;
+ * regen = the grids generated from desc, ref the targets, both
+ * (B, C, H, W, D); molecule b's atoms use grid b). */
 int vg_loss_gradient_f64(const vg_batch_desc* desc, const float* ref, const float* regen,
                          double* grad, void* stream);
 
@@ -181,6 +187,23 @@ int vg_descent_select_f64(vg_descent_state* state, const double* losses, const d
                           const float* grids, int32_t n_coords, int32_t n_steps,
                           int64_t n_voxels, int32_t patience, double* pos, double* best_pos,
                           float* regen, void* stream);
+
+/* Batched descent: n_molecules independent reversals at once. states[k],
+ * coordinates [coord_offsets[k], coord_offsets[k+1]) (device int32, 3 per
+ * atom), steps[k*n_steps + g]; molecule k's candidates are at
+ * cands[n_steps*coord_offsets[k] + g*(its coordinate count)] (the CSR order
+ * of the batched regeneration), losses[k*n_steps + g], grids[k*n_steps + g]
+ * and regen[k] (n_voxels floats each). Per molecule the same rules as the
+ * single calls, so each result equals its own single reversal. */
+int vg_descent_candidates_batch_f64(vg_descent_state* states, const int32_t* coord_offsets,
+                                    int32_t n_molecules, const double* pos, const double* grad,
+                                    const double* steps, double* cands, int32_t n_steps,
+                                    int64_t max_iters, double tolerance, void* stream);
+int vg_descent_select_batch_f64(vg_descent_state* states, const int32_t* coord_offsets,
+                                int32_t n_molecules, const double* losses, const double* cands,
+                                const float* grids, int32_t n_steps, int64_t n_voxels,
+                                int32_t patience, double* pos, double* best_pos, float* regen,
+                                void* stream);
 
 /* Device fill with 128-bit stores (HBM write-bandwidth probe for the roofline). */
 int vg_fill_f32(float* out, int64_t n, float value, void* stream);

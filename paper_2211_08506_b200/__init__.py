@@ -48,7 +48,9 @@ from .reversal import (
     loss,
     loss_gradient,
     refine_coords,
+    refine_coords_batch,
     reverse_grid,
+    reverse_grids,
 )
 from .cli import cli_main
 
@@ -106,7 +108,9 @@ __all__ = [
     "loss",
     "loss_gradient",
     "refine_coords",
+    "refine_coords_batch",
     "reverse_grid",
+    "reverse_grids",
     "cli_main",
     "__version__",
 ]

@@ -59,9 +59,11 @@ __device__ double block_reduce_f64(double v, double* red) {
 // pass 1: partial[g * kMseBlocks + blk] = sum over a fixed voxel range
 __global__ void __launch_bounds__(kMseThreads) vg_mse_partial_kernel(const float* __restrict__ ref,
                                                                      const float* __restrict__ grids,
-                                                                     int64_t n, double* partial) {
+                                                                     int64_t n, int per_ref,
+                                                                     double* partial) {
   __shared__ double red[kMseThreads / 32];
   const int g = blockIdx.y;
+  ref += (int64_t)(g / per_ref) * n;   // grids g*per_ref .. share reference g/per_ref
   const int64_t per = (n + kMseBlocks - 1) / kMseBlocks;
   const int64_t lo = (int64_t)blockIdx.x * per, hi = min(n, lo + per);
   const float* gr = grids + (int64_t)g * n;
@@ -99,6 +101,9 @@ __device__ __forceinline__ float erf_deriv_f32(float t) {
 }
 
 struct GradParams {
+  const int64_t* offsets;   // molecule b owns atoms [offsets[b], offsets[b+1]); refs/regens per molecule
+  int64_t n_mol;
+  int64_t grid_stride;      // C*H*W*D floats between molecules' grids
   const double* xyz;
   const int32_t* channel;
   const float* ref;
@@ -124,6 +129,15 @@ __global__ void __launch_bounds__(kGradThreads) vg_grad_kernel(const __grid_cons
   __shared__ double red[kGradThreads / 32];
   const int a = blockIdx.x;
   const int c = p.channel[a];
+  int64_t mol = 0;   // the molecule owning atom a (largest b with offsets[b] <= a)
+  if (p.n_mol > 1) {
+    int64_t lo = 0, hi = p.n_mol - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(p.offsets + mid) <= a) lo = mid; else hi = mid - 1;
+    }
+    mol = lo;
+  }
   for (int ax = 0; ax < 3; ++ax) {
     const int n = p.n[ax];
     const double rel = __dsub_rn(p.origin[ax], p.xyz[a * 3 + ax]);
@@ -165,8 +179,8 @@ __global__ void __launch_bounds__(kGradThreads) vg_grad_kernel(const __grid_cons
   // read once and feeds all three sums. Outside an axis' box one of its
   // factors is exactly +0, so the extra terms add nothing (d is finite).
   const int64_t slab = (int64_t)p.W * p.D;
-  const float* ref_c = p.ref + (int64_t)c * p.H * slab;
-  const float* reg_c = p.regen + (int64_t)c * p.H * slab;
+  const float* ref_c = p.ref + mol * p.grid_stride + (int64_t)c * p.H * slab;
+  const float* reg_c = p.regen + mol * p.grid_stride + (int64_t)c * p.H * slab;
   int lo[3], ext[3];
   bool empty = false;
   for (int q = 0; q < 3; ++q) {
@@ -201,12 +215,27 @@ __global__ void __launch_bounds__(kGradThreads) vg_grad_kernel(const __grid_cons
 }
 
 // --- device-resident descent (refine_coords, reversal.py:325-398) ----------
-// One CTA: the loop-top stop rules, then the backoff candidates.
-__global__ void vg_descent_cand_kernel(vg_descent_state* st, const double* __restrict__ pos,
+// One CTA per molecule k (batched reversal); molecule k's coordinates are
+// [coff[k], coff[k+1]) (coff NULL: one molecule of n_coords), its G backoff
+// candidates sit at cands[G*coff[k] + g*(coff[k+1]-coff[k]) + i] (the CSR
+// order of the regeneration batch), its steps at steps[k*G + g].
+__device__ __forceinline__ void coord_range(const int* coff, int n_coords, int k, int& lo, int& hi) {
+  lo = coff != nullptr ? coff[k] : 0;
+  hi = coff != nullptr ? coff[k + 1] : n_coords;
+}
+
+// The loop-top stop rules, then the backoff candidates.
+__global__ void vg_descent_cand_kernel(vg_descent_state* states, const int* __restrict__ coff,
+                                       int n_coords, const double* __restrict__ pos,
                                        const double* __restrict__ grad,
                                        const double* __restrict__ steps, double* __restrict__ cands,
-                                       int nc, int G, long long max_iters, double tol) {
+                                       int G, long long max_iters, double tol) {
   __shared__ int any_nz;
+  const int k = blockIdx.x;
+  vg_descent_state* st = states + k;
+  int lo, hi;
+  coord_range(coff, n_coords, k, lo, hi);
+  const int nc = hi - lo;
   if (threadIdx.x == 0) any_nz = 0;
   __syncthreads();
   if (st->done) return;   // uniform
@@ -214,7 +243,7 @@ __global__ void vg_descent_cand_kernel(vg_descent_state* st, const double* __res
   bool stop = st->iterations >= max_iters || st->current < tol;
   if (!stop) {
     bool nz = false;
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) nz = nz || grad[i] != 0.0;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) nz = nz || grad[lo + i] != 0.0;
     if (nz) any_nz = 1;
   }
   __syncthreads();
@@ -223,18 +252,24 @@ __global__ void vg_descent_cand_kernel(vg_descent_state* st, const double* __res
     if (threadIdx.x == 0) st->done = 1;
     return;
   }
+  double* out = cands + (size_t)G * lo;
   for (int i = threadIdx.x; i < G * nc; i += blockDim.x) {
-    const int g = i / nc, k = i - g * nc;
-    cands[i] = __dsub_rn(pos[k], __dmul_rn(steps[g], grad[k]));   // pos - (step0*h)*grad
+    const int g = i / nc, q = i - g * nc;
+    out[i] = __dsub_rn(pos[lo + q], __dmul_rn(steps[k * G + g], grad[lo + q]));  // pos - (step0*h)*grad
   }
 }
 
-// One CTA: first candidate (in halving order) whose loss does not exceed the
-// current one, else the smallest step; state update in the reference's order.
-__global__ void vg_descent_select_kernel(vg_descent_state* st, const double* __restrict__ losses,
-                                         const double* __restrict__ cands, int nc, int G,
-                                         int patience, double* __restrict__ pos,
-                                         double* __restrict__ best_pos) {
+// First candidate (in halving order) whose loss does not exceed the current
+// one, else the smallest step; state update in the reference's order.
+__global__ void vg_descent_select_kernel(vg_descent_state* states, const int* __restrict__ coff,
+                                         int n_coords, const double* __restrict__ losses,
+                                         const double* __restrict__ cands, int G, int patience,
+                                         double* __restrict__ pos, double* __restrict__ best_pos) {
+  const int k = blockIdx.x;
+  vg_descent_state* st = states + k;
+  int lo, hi;
+  coord_range(coff, n_coords, k, lo, hi);
+  const int nc = hi - lo;
   const bool done = st->done != 0;
   __syncthreads();
   if (done) {
@@ -242,21 +277,23 @@ __global__ void vg_descent_select_kernel(vg_descent_state* st, const double* __r
     return;
   }
   const double cur = st->current;
+  const double* lk = losses + (size_t)k * G;
   int s = G - 1;
   bool ok_any = false;
   for (int g = 0; g < G; ++g) {
-    if (losses[g] <= cur) {
+    if (lk[g] <= cur) {
       s = g;
       ok_any = true;
       break;
     }
   }
-  const double next = losses[s];
+  const double next = lk[s];
   const bool better = next < st->best;
+  const double* src = cands + (size_t)G * lo + (size_t)s * nc;
   for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-    const double v = cands[(size_t)s * nc + i];
-    pos[i] = v;
-    if (better) best_pos[i] = v;
+    const double v = src[i];
+    pos[lo + i] = v;
+    if (better) best_pos[lo + i] = v;
   }
   __syncthreads();   // every thread has read the state
   if (threadIdx.x == 0) {
@@ -273,14 +310,56 @@ __global__ void vg_descent_select_kernel(vg_descent_state* st, const double* __r
   }
 }
 
-// regen = grids[sel] after a step (grid-stride copy).
-__global__ void vg_descent_regen_kernel(const vg_descent_state* st, const float* __restrict__ grids,
-                                        float* __restrict__ regen, long long n) {
+// regen[k] = grids[k*G + sel_k] after a step (grid-stride copy, blockIdx.y = k).
+__global__ void vg_descent_regen_kernel(const vg_descent_state* states, const float* __restrict__ grids,
+                                        float* __restrict__ regen, long long n, int G) {
+  const int k = blockIdx.y;
+  const vg_descent_state* st = states + k;
   if (!st->moved) return;
-  const float* src = grids + (long long)st->sel * n;
+  const float* src = grids + ((long long)k * G + st->sel) * n;
+  float* dst = regen + (long long)k * n;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    regen[i] = src[i];
+    dst[i] = src[i];
+}
+
+}  // namespace
+
+namespace {
+
+int descent_candidates(vg_descent_state* states, const int* coff, int n_mol, int n_coords,
+                       const double* pos, const double* grad, const double* steps, double* cands,
+                       int n_steps, int64_t max_iters, double tolerance, void* stream) {
+  if (states == nullptr || pos == nullptr || grad == nullptr || steps == nullptr || cands == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates: NULL pointer");
+  if (n_mol <= 0 || (coff == nullptr && n_coords <= 0) || n_steps <= 0)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates: empty problem");
+  vg_descent_cand_kernel<<<n_mol, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      states, coff, n_coords, pos, grad, steps, cands, n_steps, (long long)max_iters, tolerance);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_descent_candidates", e);
+}
+
+int descent_select(vg_descent_state* states, const int* coff, int n_mol, int n_coords,
+                   const double* losses, const double* cands, const float* grids, int n_steps,
+                   int64_t n_voxels, int patience, double* pos, double* best_pos, float* regen,
+                   void* stream) {
+  if (states == nullptr || losses == nullptr || cands == nullptr || grids == nullptr ||
+      pos == nullptr || best_pos == nullptr || regen == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select: NULL pointer");
+  if (n_mol <= 0 || (coff == nullptr && n_coords <= 0) || n_steps <= 0 || n_voxels <= 0 ||
+      patience < 1 || n_mol > 65535)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select: bad sizes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  vg_descent_select_kernel<<<n_mol, 128, 0, st>>>(states, coff, n_coords, losses, cands, n_steps,
+                                                  patience, pos, best_pos);
+  long long blocks = (n_voxels + 255) / 256;
+  const long long cap = n_mol >= 64 ? 8 : 148 * 4 / n_mol + 1;
+  if (blocks > cap) blocks = cap;
+  vg_descent_regen_kernel<<<dim3((unsigned)blocks, (unsigned)n_mol), 256, 0, st>>>(
+      states, grids, regen, (long long)n_voxels, n_steps);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_descent_select", e);
 }
 
 }  // namespace
@@ -289,33 +368,38 @@ VG_API int vg_descent_candidates_f64(vg_descent_state* state, const double* pos,
                                      const double* steps, double* cands, int32_t n_coords,
                                      int32_t n_steps, int64_t max_iters, double tolerance,
                                      void* stream) {
-  if (state == nullptr || pos == nullptr || grad == nullptr || steps == nullptr || cands == nullptr)
-    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates_f64: NULL pointer");
-  if (n_coords <= 0 || n_steps <= 0)
-    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates_f64: empty problem");
-  vg_descent_cand_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      state, pos, grad, steps, cands, n_coords, n_steps, (long long)max_iters, tolerance);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_descent_candidates_f64", e);
+  return descent_candidates(state, nullptr, 1, n_coords, pos, grad, steps, cands, n_steps,
+                            max_iters, tolerance, stream);
 }
 
 VG_API int vg_descent_select_f64(vg_descent_state* state, const double* losses, const double* cands,
                                  const float* grids, int32_t n_coords, int32_t n_steps,
                                  int64_t n_voxels, int32_t patience, double* pos, double* best_pos,
                                  float* regen, void* stream) {
-  if (state == nullptr || losses == nullptr || cands == nullptr || grids == nullptr ||
-      pos == nullptr || best_pos == nullptr || regen == nullptr)
-    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select_f64: NULL pointer");
-  if (n_coords <= 0 || n_steps <= 0 || n_voxels <= 0 || patience < 1)
-    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select_f64: bad sizes");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  vg_descent_select_kernel<<<1, 128, 0, st>>>(state, losses, cands, n_coords, n_steps, patience, pos,
-                                              best_pos);
-  long long blocks = (n_voxels + 255) / 256;
-  if (blocks > 148 * 4) blocks = 148 * 4;
-  vg_descent_regen_kernel<<<(unsigned)blocks, 256, 0, st>>>(state, grids, regen, (long long)n_voxels);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_descent_select_f64", e);
+  return descent_select(state, nullptr, 1, n_coords, losses, cands, grids, n_steps, n_voxels,
+                        patience, pos, best_pos, regen, stream);
+}
+
+VG_API int vg_descent_candidates_batch_f64(vg_descent_state* states, const int32_t* coord_offsets,
+                                           int32_t n_molecules, const double* pos,
+                                           const double* grad, const double* steps,
+                                           double* cands, int32_t n_steps, int64_t max_iters,
+                                           double tolerance, void* stream) {
+  if (coord_offsets == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates_batch_f64: NULL offsets");
+  return descent_candidates(states, coord_offsets, n_molecules, 0, pos, grad, steps, cands,
+                            n_steps, max_iters, tolerance, stream);
+}
+
+VG_API int vg_descent_select_batch_f64(vg_descent_state* states, const int32_t* coord_offsets,
+                                       int32_t n_molecules, const double* losses,
+                                       const double* cands, const float* grids, int32_t n_steps,
+                                       int64_t n_voxels, int32_t patience, double* pos,
+                                       double* best_pos, float* regen, void* stream) {
+  if (coord_offsets == nullptr)
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select_batch_f64: NULL offsets");
+  return descent_select(states, coord_offsets, n_molecules, 0, losses, cands, grids, n_steps,
+                        n_voxels, patience, pos, best_pos, regen, stream);
 }
 
 VG_API size_t vg_mse_workspace_bytes(int64_t n_voxels, int32_t n_grids) {
@@ -323,23 +407,31 @@ VG_API size_t vg_mse_workspace_bytes(int64_t n_voxels, int32_t n_grids) {
   return (size_t)(n_grids > 0 ? n_grids : 0) * kMseBlocks * sizeof(double);
 }
 
-VG_API int vg_mse_f64(const float* ref, const float* grids, int64_t n_voxels, int32_t n_grids,
-                      double* out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (n_voxels <= 0 || n_grids < 0)
-    return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: need n_voxels > 0, n_grids >= 0");
+VG_API int vg_mse_grouped_f64(const float* refs, const float* grids, int64_t n_voxels,
+                              int32_t n_grids, int32_t grids_per_ref, double* out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (n_voxels <= 0 || n_grids < 0 || grids_per_ref < 1)
+    return vg_internal_set_error(VG_ERR_INVALID,
+                                 "vg_mse_f64: need n_voxels > 0, n_grids >= 0, grids_per_ref >= 1");
   if (n_grids == 0) return VG_OK;
-  if (ref == nullptr || grids == nullptr || out == nullptr)
+  if (refs == nullptr || grids == nullptr || out == nullptr)
     return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: NULL pointer");
   if (workspace == nullptr || workspace_bytes < vg_mse_workspace_bytes(n_voxels, n_grids))
     return vg_internal_set_error(VG_ERR_WORKSPACE, "vg_mse_f64: workspace too small");
   if (n_grids > 65535) return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: too many grids");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* partial = static_cast<double*>(workspace);
-  vg_mse_partial_kernel<<<dim3(kMseBlocks, n_grids), kMseThreads, 0, st>>>(ref, grids, n_voxels,
-                                                                            partial);
+  vg_mse_partial_kernel<<<dim3(kMseBlocks, n_grids), kMseThreads, 0, st>>>(refs, grids, n_voxels,
+                                                                            grids_per_ref, partial);
   vg_mse_final_kernel<<<n_grids, 256, 0, st>>>(partial, n_voxels, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? VG_OK : fail(VG_ERR_CUDA, "vg_mse_f64", e);
+}
+
+VG_API int vg_mse_f64(const float* ref, const float* grids, int64_t n_voxels, int32_t n_grids,
+                      double* out, void* workspace, size_t workspace_bytes, void* stream) {
+  return vg_mse_grouped_f64(ref, grids, n_voxels, n_grids, n_grids > 0 ? n_grids : 1, out,
+                            workspace, workspace_bytes, stream);
 }
 
 VG_API int vg_loss_gradient_f64(const vg_batch_desc* desc, const float* ref, const float* regen,
@@ -355,8 +447,13 @@ VG_API int vg_loss_gradient_f64(const vg_batch_desc* desc, const float* ref, con
     return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: axis longer than 1024");
   if (d.xyz == nullptr || d.channel == nullptr || !(d.scale > 0.0))
     return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: bad descriptor");
+  if (d.n_molecules < 1 || (d.n_molecules > 1 && d.offsets == nullptr))
+    return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: bad molecule count");
   GradParams p;
   memset(&p, 0, sizeof p);
+  p.offsets = d.offsets;
+  p.n_mol = d.n_molecules;
+  p.grid_stride = (int64_t)d.C * d.H * d.W * d.D;
   p.xyz = d.xyz;
   p.channel = d.channel;
   p.ref = ref;

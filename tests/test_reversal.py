@@ -184,3 +184,33 @@ def test_device_descent_equals_host_loop(max_iters, tol, graphs, monkeypatch):
         assert a.loss == b.loss
         assert a.converged == b.converged and a.diverged == b.diverged
         assert np.array_equal(a.positions, b.positions)
+
+
+@pytest.mark.gpu
+def test_batched_descent_equals_single_reversals():
+    """refine_coords_batch / reverse_grids: every molecule's result equals its
+    own refine_coords bit for bit (different atom counts, stops at different
+    iterations, a converged seed)."""
+    from paper_2211_08506_b200 import reversal as rv
+
+    grids, seeds = [], []
+    for i in range(min(4, len(REV["cases"]))):
+        rec = REV["cases"][i]
+        grids.append(_grid(rec["chans"], rec["pos"]))
+        seeds.append(vg.ReversalState(np.array(rec["chans"]), np.array(rec["cand"])))
+    exact = [[4.0, 5.0, 6.0], [8.0, 7.0, 5.5]]
+    grids.append(_grid([0, 1], exact))
+    seeds.append(vg.ReversalState(np.array([0, 1]), np.array(exact)))
+    for conf in (vg.ReversalConfig(), vg.ReversalConfig(max_iters=23, tolerance=1e-30)):
+        batch = rv.refine_coords_batch(grids, seeds, conf)
+        for g, s_, b in zip(grids, seeds, batch):
+            a = rv.refine_coords(g, s_, conf)
+            assert a.iterations == b.iterations and a.loss == b.loss
+            assert a.converged == b.converged and a.diverged == b.diverged
+            assert np.array_equal(a.positions, b.positions)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        many = rv.reverse_grids(grids)
+        for g, p in zip(grids, many):
+            one = rv.reverse_grid(g)
+            assert np.array_equal(one.to_rows(), p.to_rows())
