@@ -1907,8 +1907,36 @@ bool bin_plan(const vg_batch_desc& d, int* jc, int* nch) {
 }
 
 // K3 launch (tables must already be in the workspace, same stream).
+// K2: ordered per-(molecule, channel, y-chunk) candidate bins into the
+// workspace (layout L must carry a bin plan). Needs only the supports K1
+// wrote, so a pipeline can run it on the tables stream.
+int launch_bins(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, cudaStream_t st,
+                int* kernels) {
+  const int nb = d.C * L.bin_chunks;
+  BinParams bp;
+  bp.offsets = d.offsets;
+  bp.supp = reinterpret_cast<const int4*>(ws + L.supp);
+  bp.bins = reinterpret_cast<int*>(ws + L.bins);
+  bp.bin_off = reinterpret_cast<int*>(ws + L.bin_off);
+  bp.nb = nb;
+  bp.nch = L.bin_chunks;
+  bp.jc = L.bin_jc;
+  const size_t bsmem = (size_t)(kBinWarps + 1) * nb * sizeof(int);
+  static std::atomic<unsigned long long> configured{0};
+  if (first_on_device(configured)) {
+    cudaFuncSetAttribute(vg_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (kBinWarps + 1) * kMaxBins * (int)sizeof(int));
+  }
+  vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
+  if (kernels != nullptr) *kernels += 1;
+  return check_launch("vg_bin_kernel");
+}
+
+// bins_ready: K2 already ran for this workspace (vg_submit_f32 runs it on the
+// tables stream); otherwise it is launched here, before K3.
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
-                 vg_mol_stats* stats, cudaStream_t st, int* kernels = nullptr) {
+                 vg_mol_stats* stats, cudaStream_t st, int* kernels = nullptr,
+                 bool bins_ready = false) {
   const bool aligned16 = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   SlabPlan P;
   plan_slabs(d, aligned16, &P);
@@ -1981,28 +2009,13 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   // K2: ordered per-(molecule, channel, y-chunk) candidate bins, when the
   // workspace was laid out for this plan's chunks
   if (L.bin_jc == jc && L.bin_chunks == p.n_jchunks && L.bin_jc > 0) {
-    const int nb = d.C * p.n_jchunks;
     p.bins = reinterpret_cast<int*>(ws + L.bins);
     p.bin_off = reinterpret_cast<int*>(ws + L.bin_off);
-    p.bin_nb = nb;
-    BinParams bp;
-    bp.offsets = d.offsets;
-    bp.supp = p.supp;
-    bp.bins = reinterpret_cast<int*>(ws + L.bins);
-    bp.bin_off = reinterpret_cast<int*>(ws + L.bin_off);
-    bp.nb = nb;
-    bp.nch = p.n_jchunks;
-    bp.jc = jc;
-    const size_t bsmem = (size_t)(kBinWarps + 1) * nb * sizeof(int);
-    static std::atomic<unsigned long long> configured{0};
-    if (first_on_device(configured)) {
-      cudaFuncSetAttribute(vg_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (kBinWarps + 1) * kMaxBins * (int)sizeof(int));
+    p.bin_nb = d.C * p.n_jchunks;
+    if (!bins_ready) {
+      const int rc = launch_bins(d, L, ws, st, kernels);
+      if (rc != VG_OK) return rc;
     }
-    vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
-    if (kernels != nullptr) *kernels += 1;
-    const int rc = check_launch("vg_bin_kernel");
-    if (rc != VG_OK) return rc;
   }
   p.row_blocks = row_blocks;
   p.z_blocks = z_blocks;
@@ -2158,16 +2171,22 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (copy stage): %s", cudaGetErrorString(e));
   char* ws = static_cast<char*>(workspace);
   int kernels = 0;
+  bool bins_ready = false;
   if (B > 0 && n > 0) {
     rc = launch_tables(desc, L, ws, ts);
     if (rc != VG_OK) return rc;
     kernels = 1;
+    if (L.bin_jc > 0) {   // K2 beside the previous batch's K3 too
+      rc = launch_bins(*desc, L, ws, ts, &kernels);
+      if (rc != VG_OK) return rc;
+      bins_ready = true;
+    }
   }
   ok(cudaEventRecord(ev_tabled, ts));
   ok(cudaStreamWaitEvent(ks, ev_tabled, 0));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (tables stage): %s", cudaGetErrorString(e));
   if (B > 0) {
-    rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels);
+    rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels, bins_ready);
     if (rc != VG_OK) return rc;
     if (a->h_stats != nullptr && stats != nullptr)
       ok(cudaMemcpyAsync(a->h_stats, stats, (size_t)B * sizeof(vg_mol_stats),

@@ -628,3 +628,23 @@ def test_pipeline_edge_batches():
     r3.ready.synchronize()
     g_per, _ = vg.generate_packed(pb.offsets, pb.channels, np.mod(pb.xyz, 10.0), pspec)
     assert_bitwise(r3.grids.cpu().numpy(), g_per.cpu().numpy(), "pipeline periodic")
+
+
+def test_pipeline_binned_batches_k2_on_tables_stream():
+    """Large molecules through GridPipeline: K2 (bins) runs on the tables
+    stream next to K1, K3 reads the bins on the compute stream; bits equal the
+    serial path across slot reuse."""
+    from paper_2211_08506_b200.loader import GridPipeline, pinned_csr
+
+    cfg = synth.CONFIGS[3]
+    spec = spec_of(cfg)
+    pipe = GridPipeline(spec, depth=2)
+    batches = [synth.packed_batch(cfg, [i, i + 1]) for i in (0, 4, 9)]
+    for pb in batches:
+        before = pipe.launches
+        res = pipe.submit(*pinned_csr(pb.offsets, pb.channels, pb.xyz))
+        res.ready.synchronize()
+        assert pipe.launches - before == 3          # K1, K2, K3
+        g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+        assert_bitwise(res.grids.cpu().numpy(), g_ref.cpu().numpy(), "binned pipeline")
+        assert np.array_equal(res.stats.cpu().numpy(), s_ref.cpu().numpy())
