@@ -214,3 +214,20 @@ def test_batched_descent_equals_single_reversals():
         for g, p in zip(grids, many):
             one = rv.reverse_grid(g)
             assert np.array_equal(one.to_rows(), p.to_rows())
+
+
+def test_batched_reversal_validates_without_gpu():
+    """refine_coords_batch rejects mismatched inputs before touching the GPU."""
+    from paper_2211_08506_b200 import reversal as rv
+
+    assert rv.refine_coords_batch([], []) == []
+    import torch
+
+    g1 = vg.Grid(SPEC, torch.zeros((2,) + SPEC.shape))
+    other = vg.GridSpec(SPEC.shape, 2, vg.BoundingBox((0, 0, 0), (6, 6, 6)), 0.5)
+    g2 = vg.Grid(other, torch.zeros((2,) + SPEC.shape))
+    seeds = vg.ReversalState(np.array([0]), np.array([[1.0, 1.0, 1.0]]))
+    with pytest.raises(ValueError):
+        rv.refine_coords_batch([g1], [seeds, seeds])
+    with pytest.raises(ValueError):
+        rv.refine_coords_batch([g1, g2], [seeds, seeds])

@@ -53,7 +53,10 @@ def _worker(rank, world, port, q):
 
     dist = bench.Dist(world, rank, rank, backend="gloo")
     dist.barrier()
-    costs = np.arange(1, 101, dtype=float)
+    # bench.py --scaling strong: every rank plans the same cost-balanced cut
+    cfg = synth.CONFIGS[4]
+    costs = shard.molecule_costs(synth.atom_counts(cfg, range(100)), cfg.grid_bytes,
+                                 shard.BYTES_PER_ATOM)
     rng_ = shard.shard_range(100, rank, world, costs)
     t_max = dist.max(float(rank + 1) * 1.5)
     total = dist.sum(float(len(rng_)))
