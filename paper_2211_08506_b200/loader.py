@@ -5,19 +5,20 @@ grid tensors, overlapping the three stages of consecutive batches on
 separate CUDA streams:
 
     copy stream     H2D of batch k+1's atoms (pinned host -> device)
-    tables stream   K1 (per-atom axis tables) of batch k+1
+    tables stream   K1 (per-atom axis tables) and K2 (bins) of batch k+1
     compute stream  K3 (slab gather/store) of batch k   <- HBM-bound
 
-K1 is compute-bound and K3 HBM-bound, so running them concurrently hides
-K1 and the copies behind the grid writes. Inputs, table workspaces and
-outputs are double-buffered; every reuse waits on the event of the stage
-that last read the buffer, so results are identical to the serial path
-(bit for bit: same kernels, same inputs).
+K1/K2 are compute-bound and K3 HBM-bound, so running them concurrently
+hides most of K1 and the copies behind the grid writes. One native call per
+batch (``vg_submit_f32``) queues every stage, ordered by the slot's events.
+Inputs, table workspaces and outputs are buffered per slot (``depth``, 2 by
+default); a slot's copy stage waits for its previous K3, so results are
+identical to the serial path (bit for bit: same kernels, same inputs).
 
 The caller consumes ``result.grids`` on ``pipeline.compute_stream`` (or
-after ``result.ready.synchronize()``); a slot is rewritten two submissions
-later, after the caller's ``release`` event (optional) and the previous
-consumer-visible event.
+after ``result.ready.synchronize()``); a slot is rewritten ``depth``
+submissions later, after the caller's ``release`` event (optional) and the
+previous consumer-visible event.
 """
 
 from __future__ import annotations
