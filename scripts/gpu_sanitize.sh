@@ -1,3 +1,5 @@
+# NOTE: compute-sanitizer is closed on the shared GPU pool (it left GPUs needing resets);
+# bounds are checked instead by guard-band tests (tests/test_gpu_property.py).
 # compute-sanitizer memcheck / racecheck / synccheck over a parity subset (small inputs)
 mkdir -p gpurun_out
 SEL="(golden or window_search or bins_vs or odd_shapes or overflow or cfg0_full or pipeline_matches or pipeline_back or pipeline_edge or generic or slot_width or many_channels or fused_cta or unaligned) and not binned"

@@ -1,7 +1,9 @@
 """Randomised parity (hypothesis, 1000 + 300 derandomised cases): random shapes, channel counts, boxes,
 sigmas, thresholds, periodic cells and molecule sizes, GPU path vs the CPU
 oracle, bit for bit, with identical GenStats counters. Complements the fixed
-cases of test_gpu_parity.py with inputs nobody chose by hand."""
+cases of test_gpu_parity.py with inputs nobody chose by hand. The outputs sit
+inside guard bands that must stay untouched (bounds check in place of
+compute-sanitizer, which this GPU pool does not allow)."""
 
 from __future__ import annotations
 
@@ -56,7 +58,14 @@ def test_random_batches_match_oracle(case):
     ch = rng.integers(0, C, n).astype(np.int32)
     lattice = vg.LatticeCell(ext) if periodic else None
     spec = vg.GridSpec((H, W, D), C, vg.BoundingBox(origin, ext), sigma, lattice)
-    grids, st_ = vg.generate_packed(offsets, ch, xyz, spec, threshold=thr)
+    # output inside a guarded buffer: no kernel may write outside its grids
+    B = len(sizes)
+    n_out = B * C * H * W * D
+    guard = 4096
+    buf = torch.full((guard + n_out + guard,), -7.0, device="cuda")
+    grids = buf[guard:guard + n_out].view(B, C, H, W, D)
+    _, st_ = vg.generate_packed(offsets, ch, xyz, spec, threshold=thr, out=grids)
+    assert bool((buf[:guard] == -7.0).all()) and bool((buf[guard + n_out:] == -7.0).all())
     geom = orc.Geometry((H, W, D), C, origin, ext, sigma, periodic)
     ref, rs = orc.batch(offsets, ch, xyz, geom, threshold=thr)
     assert_bitwise(grids.cpu().numpy(), ref, f"random case {case}")
@@ -91,3 +100,41 @@ def test_random_per_molecule_boxes_match_oracle(H, W, D, C, sigma, pad, sizes, s
         assert_bitwise(got[b], ref, f"bbox case {b}")
         g, gs = res.results[b]
         assert gs.voxel_writes == rs["voxel_writes"] and gs.nonzero_voxels == rs["nonzero_voxels"]
+
+
+@pytest.mark.parametrize("k", [0, 3, 4])
+def test_workspace_and_stats_stay_in_bounds(k):
+    """Through the C-ABI: the workspace (tables, supports, K2 bins) and the
+    stats buffer sit between guard bands; vg_generate_f32 writes only inside."""
+    from paper_2211_08506_b200 import _native, synth
+
+    cfg = synth.CONFIGS[k]
+    pb = synth.packed_batch(cfg, range(3))
+    spec = vg.GridSpec(cfg.shape, cfg.channels, vg.BoundingBox(cfg.box_origin, cfg.box_extents),
+                       cfg.sigma)
+    eng = vg.GridEngine()
+    off = torch.from_numpy(pb.offsets).cuda()
+    ch = torch.from_numpy(pb.channels).cuda()
+    xyz = torch.from_numpy(pb.xyz).cuda()
+    desc = eng.describe(off, ch, xyz.view(-1, 3), spec)
+    layout = _native.VgWsLayout()
+    lib = _native.lib()
+    assert lib.vg_workspace_layout(desc, layout) == 0
+    g = 1 << 16
+    wsbuf = torch.full((g + layout.total + g,), 0xA5, dtype=torch.uint8, device="cuda")
+    stbuf = torch.full((2 * 64 + 2 * 3 + 2 * 64,), -3, dtype=torch.int64, device="cuda")
+    out = torch.empty((3, cfg.channels) + tuple(cfg.shape), device="cuda")
+    ws_ptr = wsbuf.data_ptr() + g
+    st_ptr = stbuf.data_ptr() + 2 * 64 * 8
+    rc = lib.vg_generate_f32(desc, out.data_ptr(), ws_ptr, layout.total, st_ptr,
+                             torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert bool((wsbuf[:g] == 0xA5).all()) and bool((wsbuf[g + layout.total:] == 0xA5).all())
+    assert bool((stbuf[:128] == -3).all()) and bool((stbuf[128 + 6:] == -3).all())
+    ref, rs = orc.batch(pb.offsets, pb.channels, pb.xyz,
+                        orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents,
+                                     cfg.sigma), workers=orc.host_cores())
+    assert_bitwise(out.cpu().numpy(), ref, f"guarded cfg{k}")
+    st = stbuf[128:134].view(3, 2).cpu().numpy()
+    assert [int(v) for v in st[:, 1]] == [r["nonzero_voxels"] for r in rs]
