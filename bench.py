@@ -429,6 +429,7 @@ def run_b200(args):
             ea.record(epipe.compute_stream)
             epipe.begin(ea)
             e2e_step()
+            epipe.compute_stream.wait_stream(epipe.readback_stream)   # stats on the host
             eb.record(epipe.compute_stream)
             eb.synchronize()
             wall += time.perf_counter() - w0
@@ -439,6 +440,7 @@ def run_b200(args):
         epipe.begin(ea)
         for _ in range(K):
             e2e_step()
+        epipe.compute_stream.wait_stream(epipe.readback_stream)   # last stats on the host
         eb.record(epipe.compute_stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0

@@ -100,7 +100,9 @@ int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
  *              into desc->offsets/channel/xyz, records ev_copied;
  * tables_stream waits ev_copied (hence ev_wait), K1, records ev_tabled;
  * compute_stream waits ev_tabled (hence ev_wait), K2/K3, then the D2H of the
- *              per-grid stats into h_stats (when != NULL), records ev_done.
+ *              per-grid stats into h_stats (when != NULL), records ev_done;
+ *              with a readback_stream, the D2H runs there instead, after ev_done,
+ *              followed by ev_read (K3s of consecutive batches stay back to back).
  * Events are caller-created cudaEvent_t (passed as void*); ev_wait may be
  * NULL and may be the same event as ev_done (the wait uses its previous
  * record). Returns at once: no host synchronisation. Host buffers must stay
@@ -120,6 +122,9 @@ typedef struct vg_submit_args {
   void* ev_done;
   size_t* ws_needed;
   int32_t* kernels;        /* out (if non-NULL): kernels this call launched (K1, K2, K3) */
+  void* readback_stream;   /* NULL: the stats D2H runs on compute_stream before ev_done;
+                              else on this stream after ev_done, then ev_read is recorded */
+  void* ev_read;
 } vg_submit_args;
 
 int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* args, float* out,

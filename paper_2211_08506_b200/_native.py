@@ -89,6 +89,8 @@ class VgSubmitArgs(ctypes.Structure):
         ("ev_done", ctypes.c_void_p),
         ("ws_needed", ctypes.POINTER(ctypes.c_size_t)),
         ("kernels", ctypes.POINTER(ctypes.c_int32)),
+        ("readback_stream", ctypes.c_void_p),
+        ("ev_read", ctypes.c_void_p),
     ]
 
 

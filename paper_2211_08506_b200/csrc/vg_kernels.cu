@@ -2188,11 +2188,21 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   if (B > 0) {
     rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels, bins_ready);
     if (rc != VG_OK) return rc;
-    if (a->h_stats != nullptr && stats != nullptr)
-      ok(cudaMemcpyAsync(a->h_stats, stats, (size_t)B * sizeof(vg_mol_stats),
-                         cudaMemcpyDeviceToHost, ks));
   }
+  const bool readback = B > 0 && a->h_stats != nullptr && stats != nullptr;
+  cudaStream_t rs = static_cast<cudaStream_t>(a->readback_stream);
+  cudaEvent_t ev_read = static_cast<cudaEvent_t>(a->ev_read);
+  const bool side = readback && rs != nullptr && ev_read != nullptr;
+  if (readback && !side)
+    ok(cudaMemcpyAsync(a->h_stats, stats, (size_t)B * sizeof(vg_mol_stats), cudaMemcpyDeviceToHost,
+                       ks));
   ok(cudaEventRecord(ev_done, ks));
+  if (side) {   // the read-back beside the next batch's K3
+    ok(cudaStreamWaitEvent(rs, ev_done, 0));
+    ok(cudaMemcpyAsync(a->h_stats, stats, (size_t)B * sizeof(vg_mol_stats), cudaMemcpyDeviceToHost,
+                       rs));
+    ok(cudaEventRecord(ev_read, rs));
+  }
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (compute stage): %s", cudaGetErrorString(e));
   if (a->kernels != nullptr) *a->kernels = kernels;
   return VG_OK;

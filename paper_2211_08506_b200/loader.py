@@ -55,6 +55,7 @@ class _Slot:
         self.ws_needed = ctypes.c_size_t(0)
         self.kernels = ctypes.c_int32(0)           # kernels the last submit launched
         self.used = False
+        self.read_back = False                    # last use read the stats back (ev_read)
         self._host = None
         self.out_b = -1                           # batch size `out` was allocated for
         self.ptrs = None                          # (out, ws, ws bytes, stats) pointers
@@ -81,6 +82,8 @@ class GridPipeline:
             self.copy_stream = torch.cuda.Stream(self.device)
             self.tables_stream = torch.cuda.Stream(self.device, priority=-1)
             self.compute_stream = torch.cuda.Stream(self.device)
+            # stats read-back beside the next batch's K3 (keeps K3s back to back)
+            self.readback_stream = torch.cuda.Stream(self.device)
         self.slots = [_Slot() for _ in range(depth)]
         self.k = 0
         self.launches = 0
@@ -118,7 +121,7 @@ class GridPipeline:
             for st in (self.copy_stream, self.tables_stream, self.compute_stream):
                 st.wait_event(release)
         if slot.events is None:
-            slot.events = [torch.cuda.Event() for _ in range(3)]   # copied, tabled, done
+            slot.events = [torch.cuda.Event() for _ in range(4)]   # copied, tabled, done, read
             for ev in slot.events:   # torch creates the cudaEvent_t on first record
                 ev.record(self.compute_stream)
             slot.args = _native.VgSubmitArgs()
@@ -128,12 +131,15 @@ class GridPipeline:
             slot.args.ev_copied = slot.events[0].cuda_event
             slot.args.ev_tabled = slot.events[1].cuda_event
             slot.args.ev_done = slot.events[2].cuda_event
+            slot.args.readback_stream = self.readback_stream.cuda_stream
+            slot.args.ev_read = slot.events[3].cuda_event
             slot.args.ws_needed = ctypes.pointer(slot.ws_needed)
             slot.args.kernels = ctypes.pointer(slot.kernels)
         args = slot.args
-        # the slot's previous K3 (and stats read-back) must be done before its
-        # buffers are rewritten (no wait on the slot's first use)
-        args.ev_wait = slot.events[2].cuda_event if slot.used else None
+        # the slot's previous K3 (and its stats read-back, if any) must be done
+        # before its buffers are rewritten (no wait on the slot's first use)
+        args.ev_wait = (slot.events[3] if slot.read_back else slot.events[2]).cuda_event \
+            if slot.used else None
         slot.used = True
         if (isinstance(offsets, torch.Tensor) and offsets.is_cuda and isinstance(channels, torch.Tensor)
                 and channels.is_cuda and isinstance(xyz, torch.Tensor) and xyz.is_cuda):
@@ -185,17 +191,21 @@ class GridPipeline:
             rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         _native.check(rc, "vg_submit_f32")
         self.launches += slot.kernels.value   # K1, K2 (binned batches), K3
+        slot.read_back = stats_out is not None and B > 0
+        ready = slot.events[3] if slot.read_back else slot.events[2]
         # keep the inputs alive until the copy / kernels have read them
         slot._host = host
-        return PipelineResult(slot.out, slot.stats, slot.events[2], (self.k - 1) % len(self.slots))
+        return PipelineResult(slot.out, slot.stats, ready, (self.k - 1) % len(self.slots))
 
     def begin(self, event):
         """Make every stage wait for ``event`` (e.g. the start of a timed region)."""
-        for st in (self.copy_stream, self.tables_stream, self.compute_stream):
+        for st in (self.copy_stream, self.tables_stream, self.compute_stream,
+                   self.readback_stream):
             st.wait_event(event)
 
     def synchronize(self):
-        for st in (self.copy_stream, self.tables_stream, self.compute_stream):
+        for st in (self.copy_stream, self.tables_stream, self.compute_stream,
+                   self.readback_stream):
             st.synchronize()
 
 
