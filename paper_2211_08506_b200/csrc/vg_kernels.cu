@@ -1936,7 +1936,7 @@ int launch_bins(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, cudaStr
 // tables stream); otherwise it is launched here, before K3.
 int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float* out,
                  vg_mol_stats* stats, cudaStream_t st, int* kernels = nullptr,
-                 bool bins_ready = false) {
+                 bool bins_ready = false, bool stats_zeroed = false) {
   const bool aligned16 = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   SlabPlan P;
   plan_slabs(d, aligned16, &P);
@@ -1966,7 +1966,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.C = d.C;
   p.slots_per_row = spr;
 
-  if (stats != nullptr) {
+  if (stats != nullptr && !stats_zeroed) {
     cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * d.n_molecules, st);
     if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
   }
@@ -2182,11 +2182,15 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
       bins_ready = true;
     }
   }
+  // the counters K3 accumulates start from zero: cleared here, beside the
+  // previous K3, so consecutive K3s run back to back on the compute stream
+  const bool stats_zeroed = B > 0 && stats != nullptr;
+  if (stats_zeroed) ok(cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * (size_t)B, ts));
   ok(cudaEventRecord(ev_tabled, ts));
   ok(cudaStreamWaitEvent(ks, ev_tabled, 0));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (tables stage): %s", cudaGetErrorString(e));
   if (B > 0) {
-    rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels, bins_ready);
+    rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels, bins_ready, stats_zeroed);
     if (rc != VG_OK) return rc;
   }
   const bool readback = B > 0 && a->h_stats != nullptr && stats != nullptr;
