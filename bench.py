@@ -1,10 +1,11 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 grid-generation hot path (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): per GPU, 1024 synthetic molecules of
-the config-0 distribution -> fp32 grids [1024, 5, 64, 64, 64] over a 12 A
-cube, sigma 0.5 (5.37 GB of output per step, 42x the 126 MB L2, so every
-step streams to HBM; the atom inputs are tiny and stay resident).
+Workload (BASELINE.json configs[1]): 1024 synthetic molecules of the
+config-0 distribution -> fp32 grids [1024, 5, 64, 64, 64] over a 12 A cube,
+sigma 0.5 (5.37 GB of output per step, 42x the 126 MB L2, so every step
+streams to HBM; the atom inputs are tiny and stay resident). ``--config N``
+selects another BASELINE config.
 
 A *step* = one pass of the hot path over the batch: K1 (per-atom axis
 tables) + K3 (slab gather/store, all voxels incl. zeros, fused nonzero
@@ -14,11 +15,21 @@ host (pinned) CSR inputs copied H2D and the per-grid stats read back D2H
 inside the timed region. ``roofline`` = K3's algorithmic bytes (the output)
 per launch / its CUDA-event duration vs the measured HBM peak.
 
-Multi-GPU: one process per GPU (torchrun), molecules sharded by rank with no
-collective on the data path (weak scaling: every rank generates its own
-1024-molecule batch); NCCL is used only for the barrier and the max-over-
-ranks time. ``--impl reference`` times the reference's CPU algorithm (the
-numpy oracle port, oracle/) on this host's cores instead.
+Multi-GPU: one process per GPU. ``--gpus N`` under torchrun uses the
+launcher's ranks (WORLD_SIZE must equal N); without a launcher, bench.py
+re-executes itself under ``torch.distributed.run`` with N ranks. The
+config's fixed batch is split into N cost-balanced contiguous molecule ranges
+(strong scaling, the BASELINE "single GPU then sharded over 2/4/8 GPUs";
+``--scaling weak`` gives every rank the whole batch size instead). There is
+no collective on the data path: NCCL carries only the barrier and the
+max-over-ranks time. More ranks than GPUs (plumbing runs on a 1-GPU box)
+share devices and switch the timing plumbing to gloo.
+
+``--impl reference`` times the UNMODIFIED reference (``voxgrid`` installed in
+baseline/_ref by scripts/install_reference.sh) on this host's cores: a process
+pool over the stock ``generate_grid`` on the same batch, plus the
+reference's own ``generate_batch(parallelism=ncores)``; the oracle port only
+when the install is missing.
 """
 
 from __future__ import annotations
@@ -26,7 +37,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -52,11 +65,17 @@ def parse():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", type=int, default=1, help="BASELINE config index (default 1)")
     ap.add_argument("--batch", type=int, default=None, help="molecules per GPU (default: config)")
-    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="strong",
+                    help="strong: the config's batch split over the ranks (default); "
+                         "weak: every rank processes a full batch of its own")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline budget")
-    ap.add_argument("--dist-backend", default="nccl",
-                    help="timing plumbing backend (nccl; gloo to run several ranks on one GPU)")
+    ap.add_argument("--dist-backend", default="auto",
+                    help="timing plumbing backend: auto (nccl, or gloo when ranks share GPUs), "
+                         "nccl or gloo")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="plan shards, synthesize inputs and run the timing plumbing without "
+                         "kernels (CPU test of the multi-rank path)")
     return ap.parse_args()
 
 
@@ -140,6 +159,34 @@ def dist_env():
     return world, rank, local
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """Re-execute this script under torch.distributed.run with n ranks (one
+    process per GPU); rank 0's JSON line goes to our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    log(f"[bench] --gpus {n} without a launcher: {' '.join(cmd[1:6])} ...")
+    return subprocess.call(cmd)
+
+
+def plan_indices(cfg, B, rank, world, scaling):
+    """This rank's molecule indices: a cost-balanced contiguous range of the
+    config's batch (strong), or a full batch of its own (weak)."""
+    from paper_2211_08506_b200 import shard, synth
+
+    if scaling == "weak":
+        return range(rank * B, (rank + 1) * B)
+    costs = shard.molecule_costs(synth.atom_counts(cfg, range(B)), cfg.grid_bytes,
+                                 shard.BYTES_PER_ATOM)
+    return shard.shard_range(B, rank, world, costs)
+
+
 class Dist:
     """Barrier + max/sum over ranks (timing plumbing only; no data-path
     collective). NCCL on GPUs; gloo on CPU for the multi-process tests."""
@@ -180,59 +227,179 @@ class Dist:
         self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
         return float(t.item())
 
+    def gather(self, values) -> list:
+        """Every rank's `values` (list of floats), as a list indexed by rank."""
+        vals = [float(v) for v in values]
+        if not self.pg:
+            return [vals]
+        t = self.torch.zeros((self.world, len(vals)), dtype=self.torch.float64,
+                             device=self.device)
+        t[self.rank] = self.torch.tensor(vals, dtype=self.torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return t.cpu().tolist()
+
     def close(self):
         if self.pg:
             self.td.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
-# CPU: the reference algorithm (oracle port) on this host's cores
+# CPU: the reference on this host's cores
 # ---------------------------------------------------------------------------
-def _cpu_sample(cfg, seconds: float, workers: int):
-    """Sample size for ~``seconds`` of work on ``workers`` cores (probe 8 grids)."""
+def _per_grid_seconds(cfg, fn) -> float:
+    """Serial seconds per grid of `fn(packed_batch)` on 4 molecules (probe)."""
+    from paper_2211_08506_b200 import synth
+
+    probe = synth.packed_batch(cfg, range(4))
+    t0 = time.perf_counter()
+    fn(probe)
+    return (time.perf_counter() - t0) / 4
+
+
+def _stock_grid(cfg):
+    from baseline import refbench
+
+    vx = refbench._voxgrid()
+
+    def run(pb):
+        sets, spec = refbench._build(cfg, pb)
+        for ps in sets:
+            vx.generate_grid(ps, spec)
+    return run
+
+
+def cpu_sample_size(cfg, B, workers, seconds, per_grid) -> int:
+    """Molecules for ~`seconds` of work on `workers` cores (the whole batch
+    when it fits: same_config)."""
+    return int(min(B, max(2 * workers, seconds * workers / max(per_grid, 1e-9))))
+
+
+def cpu_reference(cfg, B, seconds: float, passes: int = 2):
+    """The stock reference (baseline/_ref) as a process pool over
+    generate_grid on (a prefix of) the same batch; None if not installed."""
+    from baseline import refbench
+    from paper_2211_08506_b200 import synth
+
+    if not refbench.available():
+        return None
+    workers = refbench.host_cores()
+    n = cpu_sample_size(cfg, B, workers, seconds / max(passes, 1), _per_grid_seconds(cfg, _stock_grid(cfg)))
+    pb = synth.packed_batch(cfg, range(n))
+    rate, dt, workers = refbench.time_pool(cfg, pb, passes=passes, warmup=1, workers=workers)
+    same = n == B
+    return {"value": rate, "unit": "grids/s", "cores": workers, "kind": "reference",
+            "same_config": same,
+            "sample": (f"{'the same' if same else 'the first'} {n} molecules of {cfg.name}"
+                       f"{'' if same else f' (of {B})'}, {passes} timed passes after one untimed: "
+                       f"process pool of {workers} over the stock voxgrid.generate_grid "
+                       f"(baseline/_ref; grids dropped in the workers)"),
+            **refbench.host_info()}
+
+
+def cpu_port(cfg, B, seconds: float):
+    """The oracle port (numpy restatement) on all host cores: process pool
+    writing into shared memory."""
     from oracle import voxgrid_oracle as orc
     from paper_2211_08506_b200 import synth
 
     geom = orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents, cfg.sigma)
-    probe = synth.packed_batch(cfg, range(8))
-    t0 = time.perf_counter()
-    orc.batch(probe.offsets, probe.channels, probe.xyz, geom, workers=1)
-    per_grid = (time.perf_counter() - t0) / 8
-    n = int(max(workers * 2, min(cfg.n_molecules * 4, seconds * workers / max(per_grid, 1e-6))))
-    return geom, n
-
-
-def cpu_rate(cfg, seconds: float, workers: int):
-    """grids/s of the oracle port (the reference algorithm, numpy) over a
-    bounded sample of ``cfg``, process pool writing into shared memory."""
-    from oracle import voxgrid_oracle as orc
-    from paper_2211_08506_b200 import synth
-
-    geom, n = _cpu_sample(cfg, seconds, workers)
+    workers = orc.host_cores()
+    per = _per_grid_seconds(cfg, lambda pb: orc.batch(pb.offsets, pb.channels, pb.xyz, geom))
+    n = cpu_sample_size(cfg, B, workers, seconds, per)
     pb = synth.packed_batch(cfg, range(n))
     pool = orc.Pool(geom, n, workers)
     try:
         # warm the workers and first-touch every page of the shared output
-        # (as the reference arm's warm-up steps do), outside the timed run
         pool.run(pb.offsets, pb.channels, pb.xyz)
         t0 = time.perf_counter()
         pool.run(pb.offsets, pb.channels, pb.xyz)
         dt = time.perf_counter() - t0
     finally:
         pool.close()
-    return n / dt, n, dt
+    return {"value": n / dt, "unit": "grids/s", "cores": workers, "kind": "port",
+            "same_config": n == B,
+            "sample": f"{n} molecules of {cfg.name} in {dt:.2f}s (numpy port of "
+                      f"voxgrid.generate_grid, process pool of {workers} writing into shared memory)"}
+
+
+def cpu_baseline(cfg, B, seconds: float):
+    ref = cpu_reference(cfg, B, seconds)
+    port = cpu_port(cfg, B, min(seconds, 4.0))
+    if ref is None:
+        return port
+    ref["port"] = {k: port[k] for k in ("value", "cores", "sample")}
+    return ref
 
 
 def run_reference(args):
+    """`--impl reference`: the unmodified reference on the host cores, rank 0
+    only. Each step is one pass of the process pool over the stock
+    generate_grid on the same batch as the GPU arm (a prefix of it when the
+    whole batch would exceed ~2.5 s of CPU per step)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import voxgrid_oracle as orc
+    from baseline import refbench
     from paper_2211_08506_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
+    B = args.batch or cfg.n_molecules
+    H, W, D = cfg.shape
+    if not refbench.available():
+        return run_reference_port(args, cfg, B)
+    workers = refbench.host_cores()
+    n = cpu_sample_size(cfg, B, workers, 2.5, _per_grid_seconds(cfg, _stock_grid(cfg)))
+    pb = synth.packed_batch(cfg, range(n))
+    pool = refbench.RefPool(cfg, pb, workers)
+    try:
+        for _ in range(args.warmup):
+            pool.run()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.run()
+        dt = time.perf_counter() - t0
+    finally:
+        pool.close()
+    rate = n * args.steps / dt
+    # the reference's own parallel API on (a bounded prefix of) the same batch
+    per1 = _per_grid_seconds(cfg, _stock_grid(cfg))
+    n_gb = int(min(n, max(workers, 8.0 / max(per1, 1e-9))))
+    gb_rate, gb_dt, _ = refbench.time_generate_batch(cfg, synth.packed_batch(cfg, range(n_gb)),
+                                                     workers)
+    same = n == B
+    sample = (f"{'the same' if same else 'the first'} {n} molecules of {cfg.name} per step: "
+              f"process pool of {workers} over the stock voxgrid.generate_grid (baseline/_ref)")
+    line = {
+        "impl": "reference", "metric": "grids_per_sec", "value": rate, "unit": "grids/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "voxels_per_sec": rate * cfg.channels * H * W * D,
+        "config": {"workload": f"{cfg.name}: {n} molecules per step on the CPU",
+                   "global_batch": B, "grid": [cfg.channels, H, W, D], "sigma": cfg.sigma,
+                   "same_config": same},
+        "cpu_baseline": {"value": rate, "unit": "grids/s", "cores": workers, "kind": "reference",
+                         "sample": sample, **refbench.host_info()},
+        "reference_generate_batch": {
+            "value": gb_rate, "unit": "grids/s", "threads": workers,
+            "sample": f"voxgrid.generate_batch(parallelism={workers}) over the first {n_gb} "
+                      f"molecules in {gb_dt:.2f}s (ThreadPoolExecutor, GIL-bound)"},
+        "e2e": {"value": rate, "unit": "grids/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference_port(args, cfg, B):
+    """Reference arm without baseline/_ref: the oracle port on the host cores."""
+    from oracle import voxgrid_oracle as orc
+    from paper_2211_08506_b200 import synth
+
+    geom = orc.Geometry(cfg.shape, cfg.channels, cfg.box_origin, cfg.box_extents, cfg.sigma)
     workers = orc.host_cores()
-    geom, n = _cpu_sample(cfg, 2.5, workers)   # ~2.5 s of CPU work per step
+    per = _per_grid_seconds(cfg, lambda pb: orc.batch(pb.offsets, pb.channels, pb.xyz, geom))
+    n = cpu_sample_size(cfg, B, workers, 2.5, per)
     pb = synth.packed_batch(cfg, range(n))
     pool = orc.Pool(geom, n, workers)
     try:
@@ -247,7 +414,7 @@ def run_reference(args):
     rate = n * args.steps / dt
     H, W, D = cfg.shape
     sample = (f"{n} molecules of {cfg.name} per step (numpy port of voxgrid.generate_grid, "
-              f"process pool of {workers} writing into shared memory)")
+              f"process pool of {workers} writing into shared memory; baseline/_ref missing)")
     line = {
         "impl": "reference", "metric": "grids_per_sec", "value": rate, "unit": "grids/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -255,7 +422,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "voxels_per_sec": rate * cfg.channels * H * W * D,
         "config": {"workload": f"{cfg.name}: CPU sample of {n} molecules per step",
-                   "grid": [cfg.channels, H, W, D], "sigma": cfg.sigma},
+                   "global_batch": B, "grid": [cfg.channels, H, W, D], "sigma": cfg.sigma,
+                   "same_config": n == B},
         "cpu_baseline": {"value": rate, "unit": "grids/s", "cores": workers, "kind": "port",
                          "sample": sample},
         "e2e": {"value": rate, "unit": "grids/s", "h2d_bytes_per_step": 0,
@@ -272,21 +440,22 @@ def run_b200(args):
     import torch
 
     world, rank, local = dist_env()
-    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only for plumbing tests
+    n_dev = torch.cuda.device_count()
+    if n_dev < 1:
+        raise SystemExit("bench.py: no CUDA device (use --dry-run for the CPU plumbing test)")
+    shared = world > n_dev               # ranks share GPUs (plumbing runs on a 1-GPU box)
+    local = local % n_dev
     torch.cuda.set_device(local)
-    dist = Dist(world, rank, local, backend=args.dist_backend)
+    backend = args.dist_backend
+    if backend == "auto":
+        backend = "gloo" if shared else "nccl"   # NCCL refuses two ranks on one device
+    dist = Dist(world, rank, local, backend=backend)
     import paper_2211_08506_b200 as vg
-    from paper_2211_08506_b200 import _native, shard, synth
+    from paper_2211_08506_b200 import _native, synth
 
     cfg = synth.CONFIGS[args.config]
     B = args.batch or cfg.n_molecules
-    if args.scaling == "weak":
-        indices = range(rank * B, (rank + 1) * B)       # distinct molecules per rank
-    else:
-        # fixed total, split by rank into cost-balanced contiguous ranges
-        costs = shard.molecule_costs(synth.atom_counts(cfg, range(B)), cfg.grid_bytes,
-                                     shard.BYTES_PER_ATOM)
-        indices = shard.shard_range(B, rank, world, costs)
+    indices = plan_indices(cfg, B, rank, world, args.scaling)
     t0 = time.perf_counter()
     pb = synth.packed_batch(cfg, indices)
     log(f"[bench rank{rank}] synthesized {pb.n_molecules} molecules / {len(pb.channels)} atoms "
@@ -351,6 +520,7 @@ def run_b200(args):
     dist.barrier()
     k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
     k3_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    pairs = int(stats[:, 0].sum().item())    # P = sum of voxel_writes
     total_ms = (sum(a + b for a, b in zip(k1_ms, k3_ms)) if flush
                 else ev[0][0].elapsed_time(ev[-1][2]))
     t_max_serial = dist.max(total_ms)
@@ -470,6 +640,11 @@ def run_b200(args):
                      "api": "paper_2211_08506_b200.GaussianVoxelizer.transform(list of (m,4) "
                             "numpy arrays) + D2H of one voxel per grid"}
 
+    # per rank: molecules, pipelined ms/step, K3 ms, K3 GB/s (max-over-ranks
+    # timing is what `value` uses; this shows the balance)
+    per_rank = dist.gather([Bl, pipe_ms / K, k3_avg, achieved, len(pb.channels)])
+    sm_mhz = sampler.summary().get("sm_mhz")
+    compute = compute_leg(cfg, Bl, len(pb.channels), pairs, alg_bytes, peak, sm_mhz, dev)
     line = None
     if rank == 0:
         n_atoms = len(pb.channels)
@@ -478,6 +653,7 @@ def run_b200(args):
             "value": value,
             "unit": "grids/s",
             "n_gpus": world,
+            "ranks_per_gpu": (world + n_dev - 1) // n_dev if shared else 1,
             "steps": K,
             "warmup": max(args.warmup, 3),
             "ms_per_step": t_max / K,
@@ -487,16 +663,19 @@ def run_b200(args):
             "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32",
+            "grids_per_sec_per_gpu": value / world,
             "data": "synthetic (seeded BASELINE config distribution; no dataset)",
             "voxels_per_sec": value * cfg.channels * H * W * D,
             "config": {
-                "workload": f"{cfg.name}: {Bl} molecules/GPU -> fp32 "
-                            f"[{Bl},{cfg.channels},{H},{W},{D}], sigma {cfg.sigma}, "
-                            f"box {cfg.box_extents[0]} A",
+                "workload": f"{cfg.name}: {int(grids_total / K)} molecules -> fp32 "
+                            f"[{int(grids_total / K)},{cfg.channels},{H},{W},{D}], sigma "
+                            f"{cfg.sigma}, box {cfg.box_extents[0]} A"
+                            + (f", {args.scaling} scaling over {world} ranks" if world > 1 else ""),
                 "global_batch": int(grids_total / K),
                 "grid": [cfg.channels, H, W, D],
-                "atoms_per_gpu": n_atoms,
-                "parallelism": f"molecule-sharded x{world}, no collective",
+                "atoms_rank0": n_atoms,
+                "parallelism": f"molecule-sharded x{world} (cost-balanced contiguous ranges), "
+                               f"no collective; timing plumbing over {backend}",
                 "l2": (f"flushed: each step writes {alg_bytes / 1e6:.0f} MB, which fits the "
                        f"{l2_bytes >> 20} MB L2, so a {4 * l2_bytes >> 20} MB store stream runs "
                        "before every timed step (not timed); value and e2e are then per-step "
@@ -504,14 +683,21 @@ def run_b200(args):
                        f"no flush needed: each step writes {alg_bytes / 1e9:.2f} GB, "
                        f"> {l2_bytes >> 20} MB L2"),
             },
+            "per_rank": [{"rank": r, "molecules": int(v[0]), "atoms": int(v[4]),
+                          "ms_per_step": v[1], "grids_per_sec": v[0] / (v[1] / 1e3) if v[1] else None,
+                          "k3_ms": v[2], "k3_gbs": v[3], "k3_frac": v[3] / peak}
+                         for r, v in enumerate(per_rank)],
             "roofline": {
-                "bound": "hbm",
+                "bound": compute["bound"],
                 "kernel": "vg_slab_kernel (K3)",
+                # per GPU: rank 0's K3 (per_rank lists every GPU's)
                 "achieved": achieved,
                 "peak": peak,
                 "peak_source": peak_src,
                 "unit": "GB/s",
                 "frac": achieved / peak,
+                "frac_min_over_gpus": min(v[3] for v in per_rank) / peak,
+                "compute": compute,
                 "traffic": traffic_from_profiles(args.config),
                 "alg_bytes_per_launch": alg_bytes,
                 "k3_ms": k3_avg,
@@ -538,17 +724,37 @@ def run_b200(args):
     dist.close()
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            from oracle import voxgrid_oracle as orc
-
-            workers = orc.host_cores()
-            rate, n, dt = cpu_rate(cfg, args.cpu_seconds, workers)
-            line["cpu_baseline"] = {
-                "value": rate, "unit": "grids/s", "cores": workers, "kind": "port",
-                "sample": f"{n} molecules of {cfg.name} in {dt:.1f}s (numpy port of "
-                          f"voxgrid.generate_grid, process pool of {workers} writing into "
-                          f"shared memory)"}
+            line["cpu_baseline"] = cpu_baseline(cfg, B, args.cpu_seconds)
         print(json.dumps(line), flush=True)
     return 0
+
+
+def compute_leg(cfg, n_mol, n_atoms, pairs, alg_bytes, hbm_gbs, sm_mhz, dev):
+    """The other two legs of the north_star roofline: the FP32
+    and SFU time of the Gaussian evaluation, from the algorithmic counts
+    P = sum of voxel_writes (3 flops per pair: two multiplies and the add) and
+    E = erf_evals = atoms x ((W+1)+(H+1)+(D+1)) (~20 flops and 3 SFU ops
+    (ex2, sqrt, rcp) each), against 148 SMs x 128 FP32 lanes x 2 and 16 SFU
+    lanes per SM at the sampled SM clock. The roofline time is the largest."""
+    import torch
+
+    H, W, D = cfg.shape
+    evals = n_atoms * ((W + 1) + (H + 1) + (D + 1))
+    flops = 3 * pairs + 20 * evals
+    sfu = 3 * evals
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    ghz = (sm_mhz or 1965.0) / 1e3
+    fp32_peak = sms * 128 * 2 * ghz * 1e9
+    sfu_peak = sms * 16 * ghz * 1e9
+    t_hbm = alg_bytes / (hbm_gbs * 1e9)
+    t_fp32 = flops / fp32_peak
+    t_sfu = sfu / sfu_peak
+    bound = max((t_hbm, "hbm"), (t_fp32, "fp32"), (t_sfu, "sfu"))[1]
+    return {"bound": bound, "pairs": pairs, "erf_evals": evals, "flops": flops, "sfu_ops": sfu,
+            "t_hbm_ms": t_hbm * 1e3, "t_fp32_ms": t_fp32 * 1e3, "t_sfu_ms": t_sfu * 1e3,
+            "fp32_tflops_peak": fp32_peak / 1e12, "sfu_tops_peak": sfu_peak / 1e12,
+            "sm_count": sms, "sm_ghz": ghz}
 
 
 def traffic_from_profiles(config: int):
@@ -562,10 +768,52 @@ def traffic_from_profiles(config: int):
         return None
 
 
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without kernels (CPU, gloo): shard
+    plan, per-rank synthesis, barrier, max/sum/gather over ranks."""
+    world, rank, local = dist_env()
+    dist = Dist(world, rank, local, backend="gloo")
+    from paper_2211_08506_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    B = args.batch or cfg.n_molecules
+    indices = plan_indices(cfg, B, rank, world, args.scaling)
+    pb = synth.packed_batch(cfg, indices)
+    dist.barrier()
+    t0 = time.perf_counter()
+    checksum = float(pb.xyz.sum())
+    dt_ms = (time.perf_counter() - t0) * 1e3
+    per_rank = dist.gather([pb.n_molecules, indices.start, indices.stop, len(pb.channels), dt_ms])
+    total = dist.sum(float(pb.n_molecules))
+    t_max = dist.max(dt_ms)
+    dist.barrier()
+    if rank == 0:
+        print(json.dumps({
+            "metric": "grids_per_sec", "dry_run": True, "value": None, "unit": "grids/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "scaling": args.scaling, "global_batch": int(total), "t_max_ms": t_max,
+            "config": {"workload": cfg.name, "global_batch": int(total)},
+            "per_rank": [{"rank": r, "molecules": int(v[0]), "start": int(v[1]),
+                          "stop": int(v[2]), "atoms": int(v[3])} for r, v in enumerate(per_rank)],
+            "checksum_rank0": checksum}), flush=True)
+    dist.close()
+    return 0
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args)          # rank 0 alone, host cores
+    if env_world is None:
+        if args.gpus > 1:
+            return spawn_ranks(args.gpus)   # one process per GPU
+    elif int(env_world) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}; launch one rank per "
+              "GPU with matching counts", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return run_dry(args)
     return run_b200(args)
 
 

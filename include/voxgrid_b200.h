@@ -25,7 +25,7 @@ extern "C" {
 #define VG_ERR_CUDA -2      /* a CUDA launch or runtime call failed             */
 #define VG_ERR_WORKSPACE -3 /* workspace pointer NULL or too small              */
 
-#define VG_ABI_VERSION 3
+#define VG_ABI_VERSION 4
 
 /* One batch of molecules in CSR form plus the grid geometry.
  *
@@ -53,7 +53,12 @@ typedef struct vg_batch_desc {
 
 /* Per-molecule work counters, GenStats (gridgen.py:39-54) minus the
  * host-side fields. voxel_writes = sum over atoms of the support-box volume
- * (gridgen.py:103); nonzero_voxels = count_nonzero of the grid (gridgen.py:151). */
+ * (gridgen.py:103); nonzero_voxels = count_nonzero of the grid (gridgen.py:151).
+ * Invalid atoms — channel outside [0, C) or a non-finite coordinate, which the
+ * reference rejects with ValueError (gridgen.py:86-90, 114-119; core.py:190-199)
+ * — are never splatted and set the sign bit of their molecule's voxel_writes
+ * (voxel_writes < 0 flags the molecule; hosts validate before the launch, the
+ * flag reports device-resident inputs). */
 typedef struct vg_mol_stats {
   int64_t voxel_writes;
   int64_t nonzero_voxels;

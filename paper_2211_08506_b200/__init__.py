@@ -20,7 +20,9 @@ from .gridgen import (
     BatchResult,
     GenStats,
     GridEngine,
+    check_packed,
     default_engine,
+    flagged_molecules,
     generate_batch,
     generate_grid,
     generate_packed,
@@ -82,6 +84,8 @@ __all__ = [
     "generate_batch",
     "generate_grid",
     "generate_packed",
+    "check_packed",
+    "flagged_molecules",
     "ERF_C1",
     "ERF_C2",
     "AxisTable",

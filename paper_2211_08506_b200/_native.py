@@ -160,7 +160,7 @@ SIGNATURES = {
     "vg_abi_version": (ctypes.c_int, []),
 }
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 _lib = None
 
 

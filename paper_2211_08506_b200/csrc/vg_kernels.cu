@@ -35,6 +35,7 @@
 #include <unistd.h>   // environ
 
 #include "../../include/voxgrid_b200.h"
+#include "vg_device.cuh"
 #include "vg_math.cuh"
 
 #define VG_API extern "C" __attribute__((visibility("default")))
@@ -92,17 +93,6 @@ constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// Function attributes (dynamic shared memory limit, carveout) are set per
-// device: true the first time a kernel instance is launched on the current
-// device by any thread (setting them twice is harmless).
-bool first_on_device(std::atomic<unsigned long long>& mask) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (mask.load(std::memory_order_acquire) & bit) return false;
-  mask.fetch_or(bit, std::memory_order_acq_rel);
-  return true;
-}
 int round_up4(int v) { return (v + 3) & ~3; }
 
 // Tuning / test hooks (VG_* environment variables, read at every API call so
@@ -166,10 +156,24 @@ struct TableParams {
   int64_t n_molecules;
   int n[3];
   int row[3];
+  int C;                // channels: atoms outside [0, C) are invalid
   float threshold;
   int has_threshold;
   int periodic;
 };
+
+// An atom the reference rejects with ValueError (gridgen.py:86-90, 114-119;
+// core.py:190-199): channel outside [0, C) or a non-finite coordinate. K1
+// gives it an empty support (so K2/K3 never touch it and it adds nothing to
+// voxel_writes) and the channel marker -1, from which K3 flags its molecule
+// (vg_mol_stats.voxel_writes < 0). Hosts validate first; this keeps device
+// inputs memory-safe and their errors visible.
+__device__ __forceinline__ bool atom_invalid(const TableParams& p, int64_t atom) {
+  const int c = __ldg(p.channel + atom);
+  const double x = __ldg(p.xyz + atom * 3), y = __ldg(p.xyz + atom * 3 + 1),
+               z = __ldg(p.xyz + atom * 3 + 2);
+  return (unsigned)c >= (unsigned)p.C || !isfinite(x) || !isfinite(y) || !isfinite(z);
+}
 
 // Python float `%` for a positive divisor (kernels.py:247): fmod is exact in
 // IEEE arithmetic; the result takes the divisor's sign, +0 for exact zeros.
@@ -222,6 +226,15 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_kernel(TableParams p)
   }
   const double mu = p.xyz[atom * 3 + axis];
   const double s = p.scale;
+  if (atom_invalid(p, atom)) {   // whole row +0, empty support, channel marker -1
+    float* row = p.tbl[axis] + atom * p.row[axis];
+    for (int e = lane; e < n; e += 32) row[e] = 0.0f;
+    if (lane == 0) {
+      p.supp[atom * 4 + axis] = 0;
+      if (axis == 0) p.supp[atom * 4 + 3] = -1;
+    }
+    return;
+  }
 
   // Edge arguments are rel + delta*e (fp64) times s. Open axis: rel = o - mu
   // (kernels.py:253). Periodic: images p in (r-L, r, r+L), rel = -p, with
@@ -323,7 +336,8 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
 
   double rel = 0.0, d = 1.0;
   int glo = 0, ghi = -1;   // candidate g range (empty for invalid rows)
-  if (valid) {
+  const bool bad = valid && atom_invalid(p, atom);   // row of zeros, empty support
+  if (valid && !bad) {
     double o = p.origin[axis];
     d = p.delta[axis];
     if (p.mol_origin != nullptr || p.mol_delta != nullptr) {
@@ -441,7 +455,7 @@ __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TablePara
     const int slo = any ? nz_lo : 0;   // _support_of: (0, 0) when all zero
     const int shi = any ? nz_hi : 0;
     p.supp[atom * 4 + axis] = slo | (shi << 16);
-    if (axis == 0) p.supp[atom * 4 + 3] = p.channel[atom];
+    if (axis == 0) p.supp[atom * 4 + 3] = bad ? -1 : p.channel[atom];
   }
 }
 
@@ -496,7 +510,7 @@ struct BinParams {
   const int4* supp;
   int* bins;
   int* bin_off;
-  int nb, nch, jc;
+  int nb, nch, jc, C;
 };
 
 struct SlabShared {
@@ -685,14 +699,18 @@ __device__ void finish_stats(const SlabParams& p, SlabShared& sh, int64_t b, int
               (unsigned long long)tot);
   if (owner) {
     long long w = 0;
+    bool bad = false;
     for (int64_t a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
       const int4 s = __ldg(p.supp + a);
       w += (long long)(hi16(s.x) - lo16(s.x)) * (hi16(s.y) - lo16(s.y)) * (hi16(s.z) - lo16(s.z));
+      bad = bad || s.w < 0;   // invalid atom (K1 marker): flag the molecule
     }
     const long long wt = warp_sum(w);
     if (lane0 && wt != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[b].voxel_writes),
                 (unsigned long long)wt);
+    if (__any_sync(kFull, bad) && lane0)
+      atomicOr(reinterpret_cast<unsigned long long*>(&p.stats[b].voxel_writes), 1ull << 63);
   }
 }
 
@@ -1459,7 +1477,10 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
 // whole molecule.
 __device__ __forceinline__ void bin_range(const BinParams& p, const int4& s, int jc, bool valid,
                                           bool& member, int& c, int& k0, int& k1) {
-  member = valid && lo16(s.x) < hi16(s.x) && lo16(s.y) < hi16(s.y) && lo16(s.z) < hi16(s.z);
+  // (invalid atoms have empty supports and channel -1; the channel bound
+  // keeps q inside this warp's counters whatever the supports hold)
+  member = valid && lo16(s.x) < hi16(s.x) && lo16(s.y) < hi16(s.y) && lo16(s.z) < hi16(s.z) &&
+           (unsigned)s.w < (unsigned)p.C;
   c = s.w;
   k0 = member ? lo16(s.y) / jc : 0;
   k1 = member ? (hi16(s.y) - 1) / jc : -1;
@@ -1650,6 +1671,7 @@ int launch_tables(const vg_batch_desc* d, const vg_ws_layout& L, char* ws, cudaS
   for (int a = 0; a < 3; ++a) p.inv_delta[a] = 1.0 / d->delta[a];
   p.n_atoms = d->n_atoms;
   p.n_molecules = d->n_molecules;
+  p.C = d->C;
   p.n[0] = d->W;
   p.n[1] = d->H;
   p.n[2] = d->D;
@@ -1704,6 +1726,7 @@ VG_API int vg_workspace_layout(const vg_batch_desc* desc, vg_ws_layout* layout) 
 VG_API int vg_axis_tables_f32(const vg_batch_desc* desc, void* workspace, size_t workspace_bytes,
                               void* stream) {
   g_last_error[0] = '\0';
+  vgdev::DeviceGuard guard(workspace);
   int rc = validate(desc);
   if (rc != VG_OK) return rc;
   vg_ws_layout L;
@@ -1748,30 +1771,36 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
 }
 
 template <int M, int SW, int YP>
-void launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
+int launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   // The row kernel is register-limited to 4 CTAs/SM; ask for the largest
   // shared-memory carveout so that shared memory never lowers that.
-  static std::atomic<unsigned long long> configured{0};
-  if (first_on_device(configured)) {
-    cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         96 * 1024);
-  }
+  static vgdev::Once once;
+  const cudaError_t e = vgdev::configure_once(once, [] {
+    cudaError_t r = cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>,
+                                         cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    return r;
+  });
+  if (e != cudaSuccess)
+    return set_error(VG_ERR_CUDA, "vg_slab_kernel attributes: %s", cudaGetErrorString(e));
   vg_slab_kernel<M, SW, YP><<<grid, nt, smem, st>>>(p);
+  return VG_OK;
 }
 
 template <int SW, int YP>
-void launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
+int launch_rows(int M, dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   switch (M) {
-    case 1: launch_rows_m<1, SW, YP>(grid, nt, smem, st, p); break;
-    case 2: launch_rows_m<2, SW, YP>(grid, nt, smem, st, p); break;
-    case 3: launch_rows_m<3, SW, YP>(grid, nt, smem, st, p); break;
-    case 4: launch_rows_m<4, SW, YP>(grid, nt, smem, st, p); break;
-    case 5: launch_rows_m<5, SW, YP>(grid, nt, smem, st, p); break;
-    case 6: launch_rows_m<6, SW, YP>(grid, nt, smem, st, p); break;
-    case 7: launch_rows_m<7, SW, YP>(grid, nt, smem, st, p); break;
-    default: launch_rows_m<8, SW, YP>(grid, nt, smem, st, p); break;
+    case 1: return launch_rows_m<1, SW, YP>(grid, nt, smem, st, p);
+    case 2: return launch_rows_m<2, SW, YP>(grid, nt, smem, st, p);
+    case 3: return launch_rows_m<3, SW, YP>(grid, nt, smem, st, p);
+    case 4: return launch_rows_m<4, SW, YP>(grid, nt, smem, st, p);
+    case 5: return launch_rows_m<5, SW, YP>(grid, nt, smem, st, p);
+    case 6: return launch_rows_m<6, SW, YP>(grid, nt, smem, st, p);
+    case 7: return launch_rows_m<7, SW, YP>(grid, nt, smem, st, p);
+    default: return launch_rows_m<8, SW, YP>(grid, nt, smem, st, p);
   }
 }
 
@@ -1921,12 +1950,15 @@ int launch_bins(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, cudaStr
   bp.nb = nb;
   bp.nch = L.bin_chunks;
   bp.jc = L.bin_jc;
+  bp.C = d.C;
   const size_t bsmem = (size_t)(kBinWarps + 1) * nb * sizeof(int);
-  static std::atomic<unsigned long long> configured{0};
-  if (first_on_device(configured)) {
-    cudaFuncSetAttribute(vg_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (kBinWarps + 1) * kMaxBins * (int)sizeof(int));
-  }
+  static vgdev::Once once;
+  const cudaError_t e = vgdev::configure_once(once, [] {
+    return cudaFuncSetAttribute(vg_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (kBinWarps + 1) * kMaxBins * (int)sizeof(int));
+  });
+  if (e != cudaSuccess)
+    return set_error(VG_ERR_CUDA, "vg_bin_kernel attributes: %s", cudaGetErrorString(e));
   vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
   if (kernels != nullptr) *kernels += 1;
   return check_launch("vg_bin_kernel");
@@ -2083,14 +2115,16 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
   if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
   const dim3 grid((unsigned)ctas);
+  int rc;
   if (sw == 8 && yp == 2)
-    launch_rows<8, 2>(M, grid, nt, smem, st, p);
+    rc = launch_rows<8, 2>(M, grid, nt, smem, st, p);
   else if (sw == 8)
-    launch_rows<8, 1>(M, grid, nt, smem, st, p);
+    rc = launch_rows<8, 1>(M, grid, nt, smem, st, p);
   else if (sw == 4)
-    launch_rows<4, 1>(M, grid, nt, smem, st, p);
+    rc = launch_rows<4, 1>(M, grid, nt, smem, st, p);
   else
-    launch_rows<1, 1>(M, grid, nt, smem, st, p);
+    rc = launch_rows<1, 1>(M, grid, nt, smem, st, p);
+  if (rc != VG_OK) return rc;
   if (kernels != nullptr) *kernels += 1;
   return check_launch("vg_slab_kernel");
 }
@@ -2112,6 +2146,7 @@ int prepare(const vg_batch_desc* desc, float* out, void* workspace, size_t works
 
 VG_API int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspace,
                            size_t workspace_bytes, vg_mol_stats* stats, void* stream) {
+  vgdev::DeviceGuard guard(out);
   vg_ws_layout L;
   int rc = prepare(desc, out, workspace, workspace_bytes, &L);
   if (rc != VG_OK || desc->n_molecules == 0) return rc;
@@ -2124,6 +2159,7 @@ VG_API int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspac
 
 VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
                         size_t workspace_bytes, vg_mol_stats* stats, void* stream) {
+  vgdev::DeviceGuard guard(out);
   vg_ws_layout L;
   int rc = prepare(desc, out, workspace, workspace_bytes, &L);
   if (rc != VG_OK || desc->n_molecules == 0) return rc;
@@ -2134,6 +2170,7 @@ VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
 VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, float* out,
                          void* workspace, size_t workspace_bytes, vg_mol_stats* stats) {
   if (a == nullptr) return set_error(VG_ERR_INVALID, "submit args are NULL");
+  vgdev::DeviceGuard guard(out);
   vg_ws_layout L;
   int rc = prepare(desc, out, workspace, workspace_bytes, &L);
   if (rc == VG_ERR_WORKSPACE && a->ws_needed != nullptr) *a->ws_needed = L.total;
@@ -2217,6 +2254,7 @@ VG_API int vg_erf_f32(const float* t, float* out, int64_t n, void* stream) {
   if (n < 0) return set_error(VG_ERR_INVALID, "negative length");
   if (n == 0) return VG_OK;
   if (t == nullptr || out == nullptr) return set_error(VG_ERR_INVALID, "NULL pointer");
+  vgdev::DeviceGuard guard(out);
   const int64_t blocks64 = (n + 255) / 256;
   const unsigned blocks = (unsigned)(blocks64 > 148 * 64 ? 148 * 64 : blocks64);
   vg_erf_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(t, out, n);
@@ -2229,6 +2267,7 @@ VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
   if (n == 0) return VG_OK;
   if (out == nullptr || (reinterpret_cast<uintptr_t>(out) % 16) != 0)
     return set_error(VG_ERR_INVALID, "out must be non-NULL and 16-byte aligned");
+  vgdev::DeviceGuard guard(out);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n4 = n / 4;
   if (n4 > 0) {

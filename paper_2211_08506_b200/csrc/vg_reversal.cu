@@ -23,6 +23,7 @@
 #include <cstring>
 
 #include "../../include/voxgrid_b200.h"
+#include "vg_device.cuh"
 #include "vg_math.cuh"
 
 #define VG_API extern "C" __attribute__((visibility("default")))
@@ -334,6 +335,7 @@ int descent_candidates(vg_descent_state* states, const int* coff, int n_mol, int
     return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates: NULL pointer");
   if (n_mol <= 0 || (coff == nullptr && n_coords <= 0) || n_steps <= 0)
     return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_candidates: empty problem");
+  vgdev::DeviceGuard guard(cands);
   vg_descent_cand_kernel<<<n_mol, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       states, coff, n_coords, pos, grad, steps, cands, n_steps, (long long)max_iters, tolerance);
   cudaError_t e = cudaGetLastError();
@@ -350,6 +352,7 @@ int descent_select(vg_descent_state* states, const int* coff, int n_mol, int n_c
   if (n_mol <= 0 || (coff == nullptr && n_coords <= 0) || n_steps <= 0 || n_voxels <= 0 ||
       patience < 1 || n_mol > 65535)
     return vg_internal_set_error(VG_ERR_INVALID, "vg_descent_select: bad sizes");
+  vgdev::DeviceGuard guard(regen);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   vg_descent_select_kernel<<<n_mol, 128, 0, st>>>(states, coff, n_coords, losses, cands, n_steps,
                                                   patience, pos, best_pos);
@@ -419,6 +422,7 @@ VG_API int vg_mse_grouped_f64(const float* refs, const float* grids, int64_t n_v
   if (workspace == nullptr || workspace_bytes < vg_mse_workspace_bytes(n_voxels, n_grids))
     return vg_internal_set_error(VG_ERR_WORKSPACE, "vg_mse_f64: workspace too small");
   if (n_grids > 65535) return vg_internal_set_error(VG_ERR_INVALID, "vg_mse_f64: too many grids");
+  vgdev::DeviceGuard guard(out);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* partial = static_cast<double*>(workspace);
   vg_mse_partial_kernel<<<dim3(kMseBlocks, n_grids), kMseThreads, 0, st>>>(refs, grids, n_voxels,
@@ -449,6 +453,7 @@ VG_API int vg_loss_gradient_f64(const vg_batch_desc* desc, const float* ref, con
     return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: bad descriptor");
   if (d.n_molecules < 1 || (d.n_molecules > 1 && d.offsets == nullptr))
     return vg_internal_set_error(VG_ERR_INVALID, "vg_loss_gradient_f64: bad molecule count");
+  vgdev::DeviceGuard guard(grad);
   GradParams p;
   memset(&p, 0, sizeof p);
   p.offsets = d.offsets;

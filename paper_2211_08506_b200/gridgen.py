@@ -43,6 +43,8 @@ __all__ = [
     "generate_batch",
     "generate_packed",
     "default_engine",
+    "check_packed",
+    "flagged_molecules",
 ]
 
 _MODES = ("dense", "sparse")
@@ -160,6 +162,57 @@ def default_engine(device=None) -> GridEngine:
     return eng
 
 
+def _molecule_of(offsets: np.ndarray, atoms: np.ndarray) -> np.ndarray:
+    """Molecule index of each atom index (CSR offsets, empty molecules skipped)."""
+    return np.searchsorted(offsets, atoms, side="right") - 1
+
+
+def check_packed(offsets, channels, xyz, n_channels: int) -> None:
+    """Vectorised input validation of a host CSR batch, with the reference's
+    rules and exception type: channels in [0, C) (gridgen.py:86-87, 114-119;
+    core.py:190-191) and finite positions (gridgen.py:88-90; core.py:197-198).
+    Raises ValueError naming the first offending molecule."""
+    off = np.asarray(offsets)
+    ch = np.asarray(channels)
+    if ch.size and not (ch.min() >= 0 and ch.max() < n_channels):
+        bad = (ch < 0) | (ch >= n_channels)
+        if bad.any():
+            a = int(np.flatnonzero(bad)[0])
+            b = int(_molecule_of(off, np.array([a]))[0])
+            if int(ch[a]) < 0:
+                raise ValueError(f"molecule {b}: channel indices must be nonnegative")
+            raise ValueError(f"molecule {b}: particle channel {int(ch[a])} out of range for spec "
+                             f"with {n_channels} channels")
+    pos = np.asarray(xyz)
+    if pos.size and not np.isfinite(pos.sum()):   # fast path: a finite sum means all finite
+        fin = np.isfinite(pos.reshape(-1, 3)).all(axis=1)
+        if not fin.all():
+            a = int(np.flatnonzero(~fin)[0])
+            b = int(_molecule_of(off, np.array([a]))[0])
+            raise ValueError(f"molecule {b}: particle positions must be finite")
+
+
+def flagged_molecules(stats) -> np.ndarray:
+    """Molecules whose kernel stats carry the invalid-atom flag
+    (voxel_writes < 0: an atom with a channel outside [0, C) or a non-finite
+    position was found on the device and not splatted)."""
+    st = stats.cpu().numpy() if hasattr(stats, "cpu") else np.asarray(stats)
+    return np.flatnonzero(st[:, 0] < 0) if st.size else np.zeros(0, dtype=np.int64)
+
+
+def raise_if_flagged(stats) -> None:
+    bad = flagged_molecules(stats)
+    if bad.size:
+        raise ValueError(f"molecules {bad.tolist()[:16]} hold particles with a channel outside "
+                         "[0, C) or a non-finite position (reference ValueError, "
+                         "gridgen.py:86-90); they were not splatted")
+
+
+def _is_device(*arrs) -> bool:
+    torch = _torch()
+    return any(isinstance(a, torch.Tensor) and a.is_cuda for a in arrs)
+
+
 def _as_device(arr, dtype, device):
     torch = _torch()
     if isinstance(arr, torch.Tensor):
@@ -170,7 +223,8 @@ def _as_device(arr, dtype, device):
 
 def generate_packed(offsets, channels, xyz, spec: GridSpec, *, mol_origin=None, mol_delta=None,
                     mode: str = "sparse", threshold: float | None = None, out=None,
-                    with_stats: bool = True, device=None, stream=None, engine=None):
+                    with_stats: bool = True, device=None, stream=None, engine=None,
+                    check: bool = True):
     """CSR fast path: molecule b owns atoms ``offsets[b]:offsets[b+1]``.
 
     ``offsets`` int64 (B+1,), ``channels`` int (n,), ``xyz`` float64 (n, 3),
@@ -178,14 +232,23 @@ def generate_packed(offsets, channels, xyz, spec: GridSpec, *, mol_origin=None, 
     ``mol_delta`` (B, 3) fp64 give per-molecule boxes (x, y, z order).
     Returns ``(grids, stats)``: grids a CUDA float32 ``(B, C, H, W, D)``
     tensor, stats an int64 ``(B, 2)`` device tensor ``[voxel_writes,
-    nonzero_voxels]`` (sparse-mode support volumes) or None. Inputs are not
-    validated beyond shapes: channels must lie in [0, C) (use
-    ``generate_batch`` for per-molecule error reporting).
+    nonzero_voxels]`` (sparse-mode support volumes) or None.
+
+    Validation follows the reference (ValueError for a channel outside
+    [0, C) or a non-finite position, gridgen.py:86-90): host inputs are
+    checked on the host before the launch; device-resident inputs are
+    checked by K1, which flags the molecule (``voxel_writes < 0``) instead of
+    splatting the atom, and with ``check=True`` the flag is read back (one
+    synchronisation) and raised. ``check=False`` skips that read-back: test
+    ``stats[:, 0] < 0`` yourself (``flagged_molecules``).
     """
     torch = _torch()
     _check_mode(mode)
     eng = engine if engine is not None else default_engine(device)
     dev = eng.device
+    on_device = _is_device(offsets, channels, xyz)
+    if not on_device:
+        check_packed(offsets, channels, xyz, spec.channels)
     offsets_d = _as_device(offsets, torch.int64, dev)
     channels_d = _as_device(channels, torch.int32, dev)
     xyz_d = _as_device(xyz, torch.float64, dev).reshape(-1, 3)
@@ -203,11 +266,17 @@ def generate_packed(offsets, channels, xyz, spec: GridSpec, *, mol_origin=None, 
     elif (tuple(out.shape) != (B, spec.channels, H, W, D) or out.dtype != torch.float32
           or not out.is_contiguous() or out.device != dev):
         raise ValueError("out must be a contiguous float32 (B, C, H, W, D) tensor on the device")
-    stats = torch.empty((B, 2), dtype=torch.int64, device=dev) if with_stats else None
+    need_flag = on_device and check
+    stats = (torch.empty((B, 2), dtype=torch.int64, device=dev)
+             if with_stats or need_flag else None)
     desc = eng.describe(offsets_d, channels_d, xyz_d, spec, mol_origin=mo, mol_delta=md,
                         mode=mode, threshold=threshold)
     eng.run(desc, out, stats, stream)
-    return out, stats
+    if need_flag and B:
+        if stream is not None:
+            stream.synchronize()
+        raise_if_flagged(stats)
+    return out, (stats if with_stats else None)
 
 
 @dataclass

@@ -30,7 +30,7 @@ import numpy as np
 
 from . import _native
 from .core import GridSpec
-from .gridgen import GridEngine, _require_cuda
+from .gridgen import GridEngine, _require_cuda, check_packed, raise_if_flagged
 
 __all__ = ["GridPipeline", "PipelineResult"]
 
@@ -41,6 +41,13 @@ class PipelineResult:
     stats: object        # torch.int64 CUDA (B, 2): voxel_writes, nonzero_voxels
     ready: object        # torch.cuda.Event recorded on the compute stream
     slot: int
+
+    def check(self) -> None:
+        """Wait for the batch and raise ValueError if K1 flagged invalid atoms
+        (device-resident inputs are validated on the device: a channel
+        outside [0, C) or a non-finite position sets voxel_writes < 0)."""
+        self.ready.synchronize()
+        raise_if_flagged(self.stats)
 
 
 class _Slot:
@@ -65,10 +72,13 @@ class GridPipeline:
     """Double-buffered, three-stream generator of grid batches on one device."""
 
     def __init__(self, spec: GridSpec, device=None, mode: str = "sparse", threshold=None,
-                 depth: int = 2):
+                 depth: int = 2, validate: bool = True):
         import torch
 
         self.torch = torch
+        # host inputs are validated on the host before the copy (the
+        # reference's ValueError); device inputs by K1 (PipelineResult.check)
+        self.validate = validate
         self.device = _require_cuda(device)
         self.spec = spec
         self.mode = mode
@@ -144,15 +154,26 @@ class GridPipeline:
         if (isinstance(offsets, torch.Tensor) and offsets.is_cuda and isinstance(channels, torch.Tensor)
                 and channels.is_cuda and isinstance(xyz, torch.Tensor) and xyz.is_cuda):
             # device-resident inputs: used in place when they already have the
-            # kernel's dtypes (caller keeps them unchanged until `ready`)
+            # kernel's dtypes (caller keeps them unchanged until `ready`);
+            # conversions run on the caller's current stream
             off_d = self._dev(offsets, torch.int64)
             ch_d = self._dev(channels, torch.int32)
             xyz_d = self._dev(xyz, torch.float64)
+            # every stage follows the work already queued on the caller's
+            # stream (the producer of the inputs, or the conversions above):
+            # the copy stage waits for it, K1/K2/K3 follow the copy stage
+            self.copy_stream.wait_stream(torch.cuda.current_stream(self.device))
+            for t, src in ((off_d, offsets), (ch_d, channels), (xyz_d, xyz)):
+                if t is not src:   # our conversion: its memory must outlive the kernels
+                    t.record_stream(self.tables_stream)
+                    t.record_stream(self.compute_stream)
             args.h_offsets = args.h_channel = args.h_xyz = None
             host = (off_d, ch_d, xyz_d)
         else:
             host = (_host_array(offsets, torch.int64), _host_array(channels, torch.int32),
                     _host_array(xyz, torch.float64))
+            if self.validate:
+                check_packed(host[0].numpy(), host[1].numpy(), host[2].numpy(), spec.channels)
             slot.off = self._ensure(slot.off, B + 1, torch.int64)
             slot.ch = self._ensure(slot.ch, n, torch.int32)
             slot.xyz = self._ensure(slot.xyz, 3 * n, torch.float64)

@@ -79,3 +79,40 @@ def test_gloo_world2_shards_and_max_over_ranks():
     assert (a0, b1) == (0, 100) and b0 == a1           # disjoint, complete cover
     assert m0 == m1 == 3.0                               # max over ranks
     assert s0 == s1 == 100.0
+
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(*args, env=None, timeout=240):
+    import subprocess
+    import sys
+
+    e = {k: v for k, v in os.environ.items()
+         if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(_ROOT, "bench.py"), *args],
+                          capture_output=True, text=True, timeout=timeout, env=e, cwd=_ROOT)
+
+
+def test_bench_gpus2_spawns_two_ranks_dry_run():
+    """`bench.py --gpus 2` without a launcher re-executes itself under
+    torch.distributed.run with 2 ranks; the strong-scaling cut of cfg1's
+    1024 molecules is complete and disjoint (kernels skipped: --dry-run)."""
+    import json
+
+    res = _bench("--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "1")
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["global_batch"] == 1024 and line["scaling"] == "strong"
+    ranks = line["per_rank"]
+    assert [r["rank"] for r in ranks] == [0, 1]
+    assert ranks[0]["start"] == 0 and ranks[0]["stop"] == ranks[1]["start"]
+    assert ranks[1]["stop"] == 1024
+    assert sum(r["molecules"] for r in ranks) == 1024
+
+
+def test_bench_rejects_world_size_mismatch():
+    res = _bench("--gpus", "3", "--dry-run", env={"WORLD_SIZE": "2", "RANK": "0"})
+    assert res.returncode == 2
+    assert "WORLD_SIZE=2" in res.stderr
