@@ -83,6 +83,9 @@ constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bou
 #ifndef VG_ROW_MINB1
 #define VG_ROW_MINB1 VG_ROW_MINB   // ... for one row step per CTA (M = 1)
 #endif
+#ifndef VG_WS_MINB
+#define VG_WS_MINB 3    // K3W: resident persistent CTAs per SM the register budget targets
+#endif
 constexpr int row_minb(int m) { return m == 1 ? VG_ROW_MINB1 : VG_ROW_MINB; }
 constexpr int64_t kTaskBytes = 262144;       // K3: output bytes per CTA (y-chunk sizing)
 constexpr int64_t kFusedTaskBytes = 1048576; // ... per channel-fused CTA, all channels
@@ -93,7 +96,7 @@ constexpr int kMaxAxis = 65535;      // supports are packed in 16 bits
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-int round_up4(int v) { return (v + 3) & ~3; }
+__host__ __device__ inline int round_up4(int v) { return (v + 3) & ~3; }
 
 // Tuning / test hooks (VG_* environment variables, read at every API call so
 // that tests can switch code paths inside one process). One scan of environ
@@ -510,6 +513,7 @@ struct BinParams {
   const int4* supp;
   int* bins;
   int* bin_off;
+  int* tile_counter;   // K3W's work counter, zeroed here (K3W follows K2)
   int nb, nch, jc, C;
 };
 
@@ -951,7 +955,7 @@ template <int M, int SW, bool FIRST>
 __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int m_stride, int nj,
                                             int ibase, int row_end, int R, Counts<M> cnt,
                                             unsigned lists_s, int cap, unsigned gx_off,
-                                            unsigned gz_off, int half) {
+                                            unsigned gz_off, int half, int gy_shift) {
   using Slot = typename SlotW<SW>::T;
   const unsigned halfb = 4u * (unsigned)half;
   const int lane = (int)(threadIdx.x & 31);
@@ -969,7 +973,7 @@ __device__ __noinline__ int accumulate_rows(float* base, int64_t slab_elems, int
   float* dst_j = base;
   for (int jj = 0; jj < nj; ++jj, dst_j += slab_elems) {
     const int jbit = 1 << jj;
-    const unsigned gy_off = 4u * (unsigned)jj;
+    const unsigned gy_off = 4u * (unsigned)(jj + gy_shift);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const bool mine = ibase + m * R < row_end;
@@ -1060,7 +1064,8 @@ template <int M, int SW, bool FIRST>
 __device__ __noinline__ int accumulate_rows_pair(float* base, int64_t slab_elems, int m_stride,
                                                  int nj, int ibase, int row_end, int R,
                                                  Counts<M> cnt, unsigned lists_s, int cap,
-                                                 unsigned gx_off, unsigned gz_off, int half) {
+                                                 unsigned gx_off, unsigned gz_off, int half,
+                                                 int gy_shift) {
   using Slot = typename SlotW<SW>::T;
   const unsigned halfb = 4u * (unsigned)half;
   const int lane = (int)(threadIdx.x & 31);
@@ -1077,7 +1082,8 @@ __device__ __noinline__ int accumulate_rows_pair(float* base, int64_t slab_elems
   for (int jj = 0; jj < nj; jj += 2, dst_j += 2 * slab_elems) {
     const bool pair = jj + 1 < nj;   // uniform; an odd tail slab runs alone
     const int jbits = (pair ? 3 : 1) << jj;
-    const unsigned gy_off = 4u * (unsigned)jj;   // 8-byte aligned: jj even, blocks 16-byte aligned
+    // 8-byte aligned: jj and gy_shift even, blocks 16-byte aligned
+    const unsigned gy_off = 4u * (unsigned)(jj + gy_shift);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const bool mine = ibase + m * R < row_end;
@@ -1132,12 +1138,12 @@ template <int M, int SW, int YP, bool FIRST>
 __device__ __forceinline__ int accumulate(float* base, int64_t slab_elems, int m_stride, int nj,
                                           int ibase, int row_end, int R, Counts<M> cnt,
                                           unsigned lists_s, int cap, unsigned gx_off,
-                                          unsigned gz_off, int half) {
+                                          unsigned gz_off, int half, int gy_shift = 0) {
   if (YP == 2)
     return accumulate_rows_pair<M, SW, FIRST>(base, slab_elems, m_stride, nj, ibase, row_end, R,
-                                              cnt, lists_s, cap, gx_off, gz_off, half);
+                                              cnt, lists_s, cap, gx_off, gz_off, half, gy_shift);
   return accumulate_rows<M, SW, FIRST>(base, slab_elems, m_stride, nj, ibase, row_end, R, cnt,
-                                       lists_s, cap, gx_off, gz_off, half);
+                                       lists_s, cap, gx_off, gz_off, half, gy_shift);
 }
 
 // Asynchronous global -> shared copies (LDGSTS): a warp issues every copy of
@@ -1466,6 +1472,574 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
 }
 
 // ---------------------------------------------------------------------------
+// K3W: persistent, warp-specialised slab kernel (binned per-channel batches)
+// ---------------------------------------------------------------------------
+// The same tiles, slot layout, staged blocks, warp sublists and hot loop as
+// vg_slab_kernel, but without block-wide barriers. Each persistent CTA is one
+// producer warp and R*zw/32 consumer warps around a ring of kWsStages staged
+// "units" in shared memory:
+//   producer  takes tiles from a global counter (heaviest-first order is not
+//             needed: tiles are handed out dynamically), filters the tile's K2
+//             bin into an ordered candidate list (warp ballots, no barrier),
+//             cuts the tile's y-chunk into units whose candidates fit the
+//             staging capacity (greedy over slab pairs; a pair that does not
+//             fit is consumed in ascending candidate segments), and for each
+//             unit waits for a free ring slot (mbarrier `empty`), writes the
+//             unit's header and candidate supports, and stages every
+//             candidate's gy / gx-window / gz rows with 1-D bulk copies
+//             (cp.async.bulk, TMA engine) that complete on the slot's `full`
+//             mbarrier (expect_tx = the unit's bytes).
+//   consumers wait on `full`, build their warp-private sublists, run the hot
+//             loop and store every slot of the unit's slabs exactly once (or
+//             continue the sums of an earlier segment), then arrive on `empty`.
+// A consumer warp never waits for another consumer warp: a warp that is done
+// with a unit moves on to the next staged one, so the imbalance between the
+// dense and the empty rows of a tile no longer idles the block (the
+// `__syncthreads` stalls of vg_slab_kernel on cfg3). Every voxel still gets
+// its candidates in ascending atom order: units of one tile are produced in
+// slab order and, for the same slabs, in candidate order, and every unit is
+// consumed by every consumer warp in ring order (a thread reads back only
+// values it stored itself).
+constexpr int kWsMaxStages = 8; // ring depth (runtime, <= this)
+constexpr int kWsListCap = 512; // producer: tile candidates held per bin pass
+
+struct WsUnit {
+  int tile;    // linear tile index; -1 = no more work
+  int js, je;  // slabs [js, je) of the tile
+  int ns;      // staged candidates
+  int first;   // 1: the first candidates of these slabs (sums start at +0)
+  int gy_shift;  // js - (first staged gy slab): gy is staged from js & ~3
+  int pad0, pad1;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "VG_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra VG_WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completing `bytes` of the
+// transaction count of mbarrier `bar`. Addresses 16-byte aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// Tile geometry shared by producer and consumers: lin -> (b, c, chunk, rblk, zblk)
+// in vg_slab_kernel's per-channel order (molecule fastest).
+struct WsTile {
+  int64_t b;
+  int c, chunk, rblk, zblk;
+};
+__device__ __forceinline__ WsTile ws_decode(const SlabParams& p, int lin) {
+  WsTile T;
+  const unsigned nb = (unsigned)p.n_molecules;
+  const unsigned rest = (unsigned)lin / nb;
+  T.b = (unsigned)lin - rest * nb;
+  const unsigned tt = rest / (unsigned)p.C;
+  T.c = (int)(rest - tt * (unsigned)p.C);
+  int t = (int)tt;
+  T.zblk = t % p.z_blocks;
+  t /= p.z_blocks;
+  T.rblk = t % p.row_blocks;
+  T.chunk = t / p.row_blocks;
+  return T;
+}
+
+// Warp-cooperative ordered compaction: appends to dst (ascending source
+// order) every element of src[i0, i1) for which keep(i) holds, at most
+// `room` of them; returns how many were appended and sets `next` to the
+// first source index not examined (i1 when all were).
+template <typename Keep, typename Emit>
+__device__ __forceinline__ int warp_compact(int i0, int i1, int room, int& next, Keep keep, Emit emit) {
+  const int lane = threadIdx.x & 31;
+  int count = 0;
+  int i = i0;
+  for (; i < i1 && count < room; i += 32) {
+    const int q = i + lane;
+    const bool k = q < i1 && keep(q);
+    const unsigned bal = __ballot_sync(kFull, k);
+    const int rank = __popc(bal & ((1u << lane) - 1u));
+    const int n = __popc(bal);
+    if (count + n > room) {
+      // take only the first (room - count) hits; resume at the first one left
+      const int take = room - count;
+      if (k && rank < take) emit(count + rank, q);
+      // index of the (take)-th set bit (0-based) = first hit not taken
+      unsigned b = bal;
+      for (int r = 0; r < take; ++r) b &= b - 1u;
+      next = i + __ffs(b) - 1;
+      return room;
+    }
+    if (k) emit(count + rank, q);
+    count += n;
+  }
+  next = i < i1 ? i : i1;
+  return count;
+}
+
+#ifdef VG_EXP_WSPROF
+// Experiment builds only: cycles consumers wait for staged units / the
+// producer waits for free slots, totals, units and candidates staged.
+__device__ unsigned long long g_ws_prof[8];
+#define WSP_T0(v) long long v = clock64()
+#define WSP_ADD(i, v) atomicAdd(&g_ws_prof[i], (unsigned long long)(v))
+#else
+#define WSP_T0(v) do { } while (0)
+#define WSP_ADD(i, v) do { } while (0)
+#endif
+
+// Producer's tile filter: ordered compaction of the K2 bin entries bl[pos,
+// nbk) that pass f0 into lst (at most `room`), as {x, y, z supports, atom}.
+// U groups of 32 entries per round: all their bin loads, then all their
+// support loads are in flight at once (one warp; the two dependent global
+// loads per entry dominate otherwise). `next` = first entry not examined.
+template <int U>
+__device__ __forceinline__ int ws_scan_bin(const int* __restrict__ bl, int pos, int nbk,
+                                           const int4* __restrict__ supp, const AtomFilter& f0,
+                                           int4* lst, int room, int& next) {
+  const int lane = threadIdx.x & 31;
+  int count = 0;
+  int i = pos;
+  while (i < nbk && count < room) {
+    int at[U];
+    int4 sp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = i + u * 32 + lane;
+      at[u] = q < nbk ? __ldg(bl + q) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) sp[u] = at[u] >= 0 ? __ldg(supp + at[u]) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool k = at[u] >= 0 && f0(sp[u]);
+      const unsigned bal = __ballot_sync(kFull, k);
+      const int n = __popc(bal), rank = __popc(bal & ((1u << lane) - 1u));
+      if (count + n > room) {
+        const int take = room - count;
+        if (k && rank < take) lst[count + rank] = make_int4(sp[u].x, sp[u].y, sp[u].z, at[u]);
+        unsigned b = bal;
+        for (int r = 0; r < take; ++r) b &= b - 1u;
+        next = i + u * 32 + __ffs(b) - 1;
+        return room;
+      }
+      if (k) lst[count + rank] = make_int4(sp[u].x, sp[u].y, sp[u].z, at[u]);
+      count += n;
+    }
+    i += 32 * U;
+  }
+  next = i < nbk ? i : nbk;
+  return count;
+}
+
+// Producer-side shared state: each of the two producer warps owns a tile
+// list and its unit plan; the ring cursor and the producers' done flags are
+// handed over with the turn.
+struct WsProdShared {
+  int ring_s;             // next ring slot
+  unsigned ring_ph;       // its phase bit
+  int done[2];            // producer k found no more tiles
+  int stopped;            // the stop unit was emitted
+  int pad[3];
+};
+constexpr int kWsMaxUnits = 17;   // slab pairs per tile (jc <= 32) + 1
+
+template <int M, int NP>
+__global__ void __launch_bounds__(kRowThreads + 32 * NP, VG_WS_MINB)
+    vg_slab_ws_kernel(const __grid_constant__ SlabParams p, int* tile_counter, int n_tiles,
+                      int kWsStages) {
+  constexpr int SW = 8, YP = 2;
+  extern __shared__ float4 dyn4[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncw = (int)(blockDim.x >> 5) - NP;   // consumer warps (warps < NP produce)
+  const int cap = p.stage_cap;
+  // shared layout: full[S], empty[S], turn[2] mbarriers | WsProdShared | units[S] |
+  // meta[S][cap] int4 | stage[S][cap*stride] floats | sublists[ncw][M*cap] int2 |
+  // per producer: list[kWsListCap] int4, histograms lo/hi[2][34] int, plan[kWsMaxUnits] int2
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(dyn4);
+  WsProdShared* ps = reinterpret_cast<WsProdShared*>(bars + 2 * kWsMaxStages + 2);
+  WsUnit* units = reinterpret_cast<WsUnit*>(ps + 1);
+  int4* meta = reinterpret_cast<int4*>(units + kWsStages);
+  float* stage = reinterpret_cast<float*>(meta + kWsStages * cap);
+  const int stage_floats = cap * p.stage_stride;
+  int2* lists_all = reinterpret_cast<int2*>(stage + kWsStages * stage_floats);
+  int4* lists_prod = reinterpret_cast<int4*>(lists_all + ncw * M * cap);
+  int* hist_all = reinterpret_cast<int*>(lists_prod + 2 * kWsListCap);
+  int2* plan_all = reinterpret_cast<int2*>(hist_all + 2 * 2 * 34);
+  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + kWsMaxStages);
+  const unsigned turn0 = smem_u32(bars + 2 * kWsMaxStages);
+
+  if (tid == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(full0 + 8u * s, 1);
+      mbar_init(empty0 + 8u * s, (unsigned)ncw);
+    }
+    mbar_init(turn0, 1);
+    mbar_init(turn0 + 8u, 1);
+    ps->ring_s = 0;
+    ps->ring_ph = 0;
+    ps->done[0] = 0;
+    ps->done[1] = NP == 1 ? 1 : 0;   // one producer: it keeps the turn from the start
+    ps->stopped = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();   // the only block-wide barrier
+
+  const int zw = p.zw, R = p.rows_per_step;
+  const int64_t chan_elems = (int64_t)p.H * p.slab_elems;
+
+  if (warp < NP) {
+    // ------------------------------------------------------------ producers
+    // Two producer warps take turns: while one emits its tile's units into
+    // the ring (the serial part), the other fetches the next tile and scans
+    // its bin (dependent global loads: the latency that would otherwise
+    // leave the consumers waiting). Turn k is an mbarrier the other producer
+    // arrives on; the ring cursor travels with the turn.
+#ifdef VG_EXP_WSPROF
+    const long long tp0 = clock64();
+#endif
+    const int k = warp;
+    int4* list = lists_prod + k * kWsListCap;
+    int* hlo = hist_all + k * 68;    // [34]: candidates whose (relative) y-support starts at j
+    int* hhi = hlo + 34;             // [34]: ... ends at j
+    int2* plan = plan_all + k * kWsMaxUnits;
+    const unsigned my_turn = turn0 + 8u * k, other_turn = turn0 + 8u * (k ^ 1);
+    unsigned turn_par = k == 0 ? 1u : 0u;   // producer 0 holds the first turn
+    bool hold = false;                      // kept the turn (other producer is done)
+    const unsigned gz_bytes = 4u * (unsigned)(zw * SW);
+    int next_tile = 0;
+    if (lane == 0) next_tile = atomicAdd(tile_counter, 1);
+    for (;;) {
+      const int tile = __shfl_sync(kFull, next_tile, 0);
+      const bool valid = tile < n_tiles;
+      WsTile T{};
+      int j0 = 0, j1 = 0, row_base = 0, row_end = 0, zv0 = 0, nl = 0, pos = 0, nbk = 0, n_units = 0;
+      const int* bl = nullptr;
+      AtomFilter f0{};
+      const bool gx16 = true;   // row_base % 4 == 0 (launch rule)
+      // gx window start | staged count << 16 of a candidate (staged bulk copy)
+      auto gx_pack = [&](int sx) {
+        const int g0 = gx_window_start(p, sx, row_base, gx16);
+        const int cnt = p.gx_win > 0 ? min(p.gx_win, p.rx - g0) : round_up4(row_end - row_base);
+        return g0 | (cnt << 16);
+      };
+      // candidates of list[0, nl) -> histograms -> unit plan (slab pairs, greedy)
+      auto make_plan = [&]() {
+        const int nj = j1 - j0;
+        for (int j = lane; j < 68; j += 32) hlo[j] = 0;
+        __syncwarp();
+        for (int i = lane; i < nl; i += 32) {
+          const int sy = list[i].y;
+          atomicAdd(&hlo[max(lo16(sy) - j0, 0)], 1);
+          atomicAdd(&hhi[min(hi16(sy) - j0, nj)], 1);
+        }
+        __syncwarp();
+        if (lane == 0) {   // suffix sums of starts (#lo >= j), prefix sums of ends (#hi <= j)
+          int run = 0;
+          for (int j = nj; j >= 0; --j) { run += hlo[j]; hlo[j] = run; }
+          run = 0;
+          for (int j = 0; j <= nj; ++j) { run += hhi[j]; hhi[j] = run; }
+        }
+        __syncwarp();
+        // count(js, je) = nl - #(lo >= je) - #(hi <= js)
+        int nu = 0, js = 0;
+        while (js < nj) {
+          int je = min(nj, js + 2);
+          while (je < nj) {
+            const int je2 = min(nj, je + 2);
+            if (nl - hlo[je2] - hhi[js] > cap) break;
+            je = je2;
+          }
+          if (lane == 0) plan[nu] = make_int2(js, je);
+          ++nu;
+          js = je;
+        }
+        __syncwarp();
+        return nu;
+      };
+      if (valid) {
+        T = ws_decode(p, tile);
+        const int64_t a0 = __ldg(p.offsets + T.b), a1 = __ldg(p.offsets + T.b + 1);
+        j0 = T.chunk * p.jc;
+        j1 = min(p.H, j0 + p.jc);
+        row_base = T.rblk * M * R;
+        row_end = min(p.W, row_base + M * R);
+        zv0 = T.zblk * zw * SW;
+        const int zv1 = min(p.D, zv0 + zw * SW);
+        if (p.stats != nullptr && T.c == 0 && T.chunk == 0 && T.rblk == 0 && T.zblk == 0) {
+          // voxel_writes (gridgen.py:103) and the invalid-atom flag of the molecule
+          long long w = 0;
+          bool bad = false;
+          for (int64_t a = a0 + lane; a < a1; a += 32 * 8) {
+            int4 sp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)   // 8 loads in flight per lane
+              sp[u] = a + 32 * u < a1 ? __ldg(p.supp + a + 32 * u) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              w += (long long)(hi16(sp[u].x) - lo16(sp[u].x)) * (hi16(sp[u].y) - lo16(sp[u].y)) *
+                   (hi16(sp[u].z) - lo16(sp[u].z));
+              bad = bad || sp[u].w < 0;
+            }
+          }
+          const long long wt = warp_sum(w);
+          if (lane == 0 && wt != 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[T.b].voxel_writes),
+                      (unsigned long long)wt);
+          if (__any_sync(kFull, bad) && lane == 0)
+            atomicOr(reinterpret_cast<unsigned long long*>(&p.stats[T.b].voxel_writes), 1ull << 63);
+        }
+        // the tile's K2 bin: ordered atoms of channel c whose y-support meets the chunk
+        const int* bo = p.bin_off + T.b * (p.bin_nb + 1) + T.c * p.n_jchunks + T.chunk;
+        const int q0 = __ldg(bo);
+        nbk = __ldg(bo + 1) - q0;
+        bl = p.bins + a0 * p.n_jchunks + q0;
+        f0 = AtomFilter{T.c, j0, j1, row_base, row_end, zv0, zv1};
+        int nxt = nbk;
+        nl = ws_scan_bin<4>(bl, 0, nbk, p.supp, f0, list, kWsListCap, nxt);
+        pos = nxt;
+        __syncwarp();
+        for (int i = lane; i < nl; i += 32) list[i].z = gx_pack(list[i].x);
+        __syncwarp();
+        n_units = make_plan();
+        if (lane == 0) next_tile = atomicAdd(tile_counter, 1);   // in flight during the turn
+      }
+      // ---- take the turn (the ring is ours until we pass it on)
+      if (!hold) {
+        mbar_wait(my_turn, turn_par);
+        turn_par ^= 1u;
+      }
+      const bool other_done = ps->done[k ^ 1] != 0;
+      int s = ps->ring_s;
+      unsigned ph = ps->ring_ph;
+      if (!valid) {
+        if (other_done) {   // last producer standing: the stop unit
+          mbar_wait(empty0 + 8u * s, ph ^ 1u);
+          if (lane == 0) {
+            units[s].tile = -1;
+            mbar_arrive(full0 + 8u * s);
+          }
+        } else if (lane == 0) {
+          ps->done[k] = 1;
+          mbar_arrive(other_turn);
+        }
+        break;
+      }
+      int pass = 0;
+      for (;;) {
+        for (int ui = 0; ui < n_units; ++ui) {
+          const int2 pu = plan[ui];
+          const int js = j0 + pu.x, je = j0 + pu.y;
+          const int gy0 = js & ~3;
+          const unsigned gy_bytes = 4u * (unsigned)(round_up4(je) - gy0);
+          int kc = 0, seg = 0;
+          for (;;) {
+#ifdef VG_EXP_WSPROF
+            const long long tw = clock64();
+            mbar_wait(empty0 + 8u * s, ph ^ 1u);
+            if (lane == 0) { WSP_ADD(2, clock64() - tw); WSP_ADD(4, 1); }
+#else
+            mbar_wait(empty0 + 8u * s, ph ^ 1u);
+#endif
+            int4* um = meta + s * cap;
+            // ordered compaction of the candidates meeting [js, je), from kc
+            unsigned bytes = 0;
+            int ns = 0, i = kc;
+            for (; i < nl && ns < cap; i += 32) {
+              const int q = i + lane;
+              int4 e = make_int4(0, 0, 0, 0);
+              bool hit = false;
+              if (q < nl) {
+                e = list[q];
+                hit = lo16(e.y) < je && hi16(e.y) > js;
+              }
+              const unsigned bal = __ballot_sync(kFull, hit);
+              const int n = __popc(bal), rank = __popc(bal & ((1u << lane) - 1u));
+              if (ns + n > cap) {   // take the first cap - ns hits, resume at the next one
+                const int take = cap - ns;
+                if (hit && rank < take) {
+                  um[ns + rank] = e;
+                  bytes += gy_bytes + gz_bytes + 4u * (unsigned)hi16(e.z);
+                }
+                unsigned b = bal;
+                for (int r = 0; r < take; ++r) b &= b - 1u;
+                i += __ffs(b) - 1;   // the first hit not taken
+                ns = cap;
+                break;
+              }
+              if (hit) {
+                um[ns + rank] = e;
+                bytes += gy_bytes + gz_bytes + 4u * (unsigned)hi16(e.z);
+              }
+              ns += n;
+            }
+            kc = i < nl ? i : nl;
+            bytes = __reduce_add_sync(kFull, bytes);
+            if (lane == 0) {
+              units[s].tile = tile;
+              units[s].js = js;
+              units[s].je = je;
+              units[s].ns = ns;
+              units[s].first = (pass == 0 && seg == 0) ? 1 : 0;
+              units[s].gy_shift = js - gy0;
+            }
+            __syncwarp();
+            const unsigned fb = full0 + 8u * s;
+            if (lane == 0) {
+              if (bytes != 0) mbar_arrive_tx(fb, bytes);
+              else mbar_arrive(fb);
+            }
+            __syncwarp();
+            const unsigned blk0 = smem_u32(stage + s * stage_floats);
+            for (int q = lane; q < ns; q += 32) {
+              const int4 e = um[q];
+              const int64_t a = e.w;
+              const unsigned d0 = blk0 + 4u * (unsigned)(q * p.stage_stride);
+              bulk_g2s(d0, p.ty + a * p.ry + gy0, gy_bytes, fb);
+              bulk_g2s(d0 + 4u * (unsigned)p.stage_gx, p.tx + a * p.rx + lo16(e.z),
+                       4u * (unsigned)hi16(e.z), fb);
+              bulk_g2s(d0 + 4u * (unsigned)p.stage_gz, p.tz + a * p.rz + zv0, gz_bytes, fb);
+            }
+            if (++s == kWsStages) {
+              s = 0;
+              ph ^= 1u;
+            }
+            ++seg;
+            if (kc >= nl) break;
+          }
+        }
+        if (pos >= nbk) break;
+        // more than kWsListCap candidates in the bin (rare): the next ones,
+        // continuing every voxel's sum (first = 0), while holding the turn
+        ++pass;
+        int nxt = nbk;
+        nl = ws_scan_bin<4>(bl, pos, nbk, p.supp, f0, list, kWsListCap, nxt);
+        pos = nxt;
+        __syncwarp();
+        for (int i = lane; i < nl; i += 32) list[i].z = gx_pack(list[i].x);
+        __syncwarp();
+        n_units = make_plan();
+      }
+      // ---- pass the turn (keep it when the other producer has finished)
+      if (lane == 0) {
+        ps->ring_s = s;
+        ps->ring_ph = ph;
+      }
+      __syncwarp();
+      if (other_done) {
+        hold = true;
+      } else {
+        if (lane == 0) mbar_arrive(other_turn);
+      }
+    }
+#ifdef VG_EXP_WSPROF
+    if (lane == 0) WSP_ADD(3, clock64() - tp0);
+#endif
+    return;
+  }
+
+  // --------------------------------------------------------------- consumers
+  const int ct = tid - 32 * NP, cw = warp - NP;
+  const int r0 = div_magic(ct, p.zw_magic);
+  const int kk = ct - r0 * zw;                       // slot in the z window
+  const int wr0 = div_magic(cw * 32, p.zw_magic), wr1 = div_magic(cw * 32 + 31, p.zw_magic);
+  const int half = 4 * zw;
+  const unsigned gz_off = 4u * (unsigned)(p.stage_gz + 4 * kk);
+  const unsigned gx_off = 4u * (unsigned)(p.stage_gx + r0);
+  int2* lists = lists_all + cw * M * cap;
+  const unsigned lists_s = smem_u32(lists);
+  int s = 0;
+  unsigned ph = 0;
+  // nonzero counts are flushed per tile (one warp atomic), not per unit
+  int64_t nz_b = -1;
+  long long nz_acc = 0;
+  auto flush = [&]() {
+    const long long tot = warp_sum(nz_acc);
+    if (lane == 0 && tot != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.stats[nz_b].nonzero_voxels),
+                (unsigned long long)tot);
+    nz_acc = 0;
+  };
+  int cur_tile = -1;
+#ifdef VG_EXP_WSPROF
+  const long long tc0 = clock64();
+  long long waited = 0;
+#endif
+  for (;;) {
+#ifdef VG_EXP_WSPROF
+    const long long tw = clock64();
+    mbar_wait(full0 + 8u * s, ph);
+    waited += clock64() - tw;
+#else
+    mbar_wait(full0 + 8u * s, ph);
+#endif
+    const WsUnit u = units[s];
+#ifdef VG_EXP_WSPROF
+    if (lane == 0 && cw == 0 && u.tile >= 0) WSP_ADD(5, u.ns);
+#endif
+    if (u.tile < 0) break;
+    const WsTile T = ws_decode(p, u.tile);
+    if (u.tile != cur_tile) {
+      if (p.stats != nullptr && nz_b >= 0) flush();
+      cur_tile = u.tile;
+      nz_b = T.b;
+    }
+    const int row_base = T.rblk * M * R, row_end = min(p.W, row_base + M * R);
+    const int zv0 = T.zblk * zw * SW;
+    const int ibase = row_base + r0;
+    const int zf = zv0 + 4 * kk;
+    const int rlo0 = row_base + wr0, rhi0 = row_base + wr1;
+    const unsigned stage_s = smem_u32(stage + s * stage_floats);
+    Counts<M> cnt;
+    build_sublists<M>(p, meta + s * cap, u.ns, -1, lists, stage_s, u.js, u.je, row_base, rlo0, rhi0,
+                      R, cnt);
+    __syncwarp();
+    float* base = p.out + (T.b * p.C + T.c) * chan_elems + u.js * p.slab_elems + ibase * p.D + zf;
+    int nz;
+    if (u.first)
+      nz = accumulate<M, SW, YP, true>(base, p.slab_elems, R * p.D, u.je - u.js, ibase, row_end, R, cnt,
+                                       lists_s, cap, gx_off, gz_off, half, u.gy_shift);
+    else
+      nz = accumulate<M, SW, YP, false>(base, p.slab_elems, R * p.D, u.je - u.js, ibase, row_end, R,
+                                        cnt, lists_s, cap, gx_off, gz_off, half, u.gy_shift);
+    __syncwarp();   // every lane is done reading the slot's staged data
+    if (lane == 0) mbar_arrive(empty0 + 8u * s);
+    nz_acc += nz;
+    if (++s == kWsStages) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+  if (p.stats != nullptr && nz_b >= 0) flush();
+#ifdef VG_EXP_WSPROF
+  if (lane == 0) {
+    WSP_ADD(0, waited);
+    WSP_ADD(1, clock64() - tc0);
+  }
+#endif
+}
+
+// ---------------------------------------------------------------------------
 // K2: ordered candidate bins for large molecules
 // ---------------------------------------------------------------------------
 // One CTA per molecule. Bin q = channel * nch + y-chunk holds, in ascending
@@ -1494,6 +2068,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) vg_bin_kernel(const __grid_con
   const int64_t b = blockIdx.x;
   const int64_t a0 = __ldg(p.offsets + b), a1 = __ldg(p.offsets + b + 1);
   const int nb = p.nb, nch = p.nch;
+  if (b == 0 && threadIdx.x == 0 && p.tile_counter != nullptr) *p.tile_counter = 0;
   for (int i = threadIdx.x; i < kBinWarps * nb; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   const int64_t n = a1 - a0;
@@ -1644,7 +2219,9 @@ void fill_layout(const vg_batch_desc* d, vg_ws_layout* L) {
     L->bins = off;
     off = align_up(off + na * (size_t)nch * sizeof(int32_t), 256);
     L->bin_off = off;
-    off = align_up(off + (size_t)d->n_molecules * ((size_t)d->C * nch + 1) * sizeof(int32_t), 256);
+    // bin offsets, then K3W's tile counter (16-byte aligned, see tile_counter_of)
+    off = align_up(off + (size_t)d->n_molecules * ((size_t)d->C * nch + 1) * sizeof(int32_t) + 32,
+                   256);
   }
   L->total = off == 0 ? 256 : off;
 }
@@ -1939,10 +2516,17 @@ bool bin_plan(const vg_batch_desc& d, int* jc, int* nch) {
 // K2: ordered per-(molecule, channel, y-chunk) candidate bins into the
 // workspace (layout L must carry a bin plan). Needs only the supports K1
 // wrote, so a pipeline can run it on the tables stream.
+// K3W's tile counter: after the bin offsets, in the same workspace region.
+int* tile_counter_of(const vg_batch_desc& d, const vg_ws_layout& L, char* ws) {
+  const size_t n = (size_t)d.n_molecules * ((size_t)d.C * L.bin_chunks + 1) * sizeof(int32_t);
+  return reinterpret_cast<int*>(ws + L.bin_off + align_up(n, 16));
+}
+
 int launch_bins(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, cudaStream_t st,
                 int* kernels) {
   const int nb = d.C * L.bin_chunks;
   BinParams bp;
+  bp.tile_counter = tile_counter_of(d, L, ws);
   bp.offsets = d.offsets;
   bp.supp = reinterpret_cast<const int4*>(ws + L.supp);
   bp.bins = reinterpret_cast<int*>(ws + L.bins);
@@ -1962,6 +2546,73 @@ int launch_bins(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, cudaStr
   vg_bin_kernel<<<(unsigned)d.n_molecules, kBinWarps * 32, bsmem, st>>>(bp);
   if (kernels != nullptr) *kernels += 1;
   return check_launch("vg_bin_kernel");
+}
+
+template <int M, int NP>
+int launch_ws_m(int grid, int threads, size_t smem, cudaStream_t st, const SlabParams& p,
+                int* counter, int n_tiles, int stages) {
+  static vgdev::Once once;
+  const cudaError_t e = vgdev::configure_once(once, [] {
+    return cudaFuncSetAttribute(vg_slab_ws_kernel<M, NP>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (e != cudaSuccess)
+    return set_error(VG_ERR_CUDA, "vg_slab_ws_kernel attributes: %s", cudaGetErrorString(e));
+  vg_slab_ws_kernel<M, NP><<<grid, threads, smem, st>>>(p, counter, n_tiles, stages);
+  return check_launch("vg_slab_ws_kernel");
+}
+
+// SM count of the current device (cached per device).
+int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// K3W launch: staged block per candidate gy[pad4(jc + 5)] (a unit's slabs
+// from js & ~3) | gx window | gz window; staging capacity from the shared
+// memory of VG_WS_MINB resident CTAs; one persistent CTA per slot.
+int launch_ws(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, SlabParams& p, int M, int R,
+              int nt, int jc, cudaStream_t st) {
+  p.stage_gx = round_up4(jc + 5);
+  p.stage_gz = p.stage_gx + (p.gx_win > 0 ? p.gx_win : round_up4(M * R));
+  p.stage_stride = p.stage_gz + round_up4(p.zw * 8);
+  p.c0_cap = 0;
+  const int ncw = nt / 32;
+  const int np = env_int("VG_WS_NP", 1, 1, 2);             // producer warps
+  const int kWsStages = env_int("VG_WS_STAGES", 4, 2, kWsMaxStages);
+  const int64_t fixed = (2 * kWsMaxStages + 2) * 8 + (int64_t)sizeof(WsProdShared) +
+                        kWsStages * (int64_t)sizeof(WsUnit) + 2 * (int64_t)kWsListCap * 16 +
+                        2 * 68 * 4 + 2 * kWsMaxUnits * 8;
+  const int64_t per_cand = kWsStages * (16 + 4 * (int64_t)p.stage_stride) + (int64_t)ncw * M * 8;
+  const int blocks = env_int("VG_WS_CTAS", VG_WS_MINB, 1, 8);
+  const int64_t budget = (int64_t)228 * 1024 / blocks - 1024 - fixed;
+  int64_t cap = budget / per_cand;
+  cap = cap > kListCap ? kListCap : cap;
+  cap = env_int("VG_WS_CAP", (int)cap, 8, (int)cap) & ~1;   // even: keeps the layout 16-byte aligned
+  if (cap < 8) return set_error(VG_ERR_INVALID, "K3W: staging rows too long");
+  p.stage_cap = (int)cap;
+  p.stage_floats = 0;
+  const size_t smem = (size_t)(fixed + cap * per_cand);
+  const int64_t n_tiles64 = d.n_molecules * (int64_t)d.C * p.tasks;
+  if (n_tiles64 > INT_MAX) return set_error(VG_ERR_INVALID, "too many tiles (%lld)", (long long)n_tiles64);
+  const int n_tiles = (int)n_tiles64;
+  int grid = sm_count() * blocks;
+  if (grid > n_tiles) grid = n_tiles;
+  int* counter = tile_counter_of(d, L, ws);
+  const int th = nt + 32 * np;
+  if (np == 1)
+    return M == 1 ? launch_ws_m<1, 1>(grid, th, smem, st, p, counter, n_tiles, kWsStages)
+                  : launch_ws_m<2, 1>(grid, th, smem, st, p, counter, n_tiles, kWsStages);
+  return M == 1 ? launch_ws_m<1, 2>(grid, th, smem, st, p, counter, n_tiles, kWsStages)
+                : launch_ws_m<2, 2>(grid, th, smem, st, p, counter, n_tiles, kWsStages);
 }
 
 // bins_ready: K2 already ran for this workspace (vg_submit_f32 runs it on the
@@ -2069,6 +2720,28 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     }
   }
   if (env_int("VG_GXWIN", 1, 0, 1) == 0) p.gx_win = 0;
+  // Binned per-channel batches (large molecules): the persistent,
+  // warp-specialised K3W when its alignment rules hold (8-voxel slots and
+  // slab pairs, even y-chunks so every unit starts on an even slab, 16-byte
+  // aligned x rows for the bulk copies). VG_WS=0 keeps vg_slab_kernel.
+  if (p.bins != nullptr && !fuse && sw == 8 && yp == 2 && M <= 2 && jc % 2 == 0 &&
+      (M * R) % 4 == 0 && env_int("VG_WS", 0, 0, 1) == 1) {
+    // VG_WS_M=2: two row steps per tile (twice the rows per producer pass)
+    int Mw = M, rbw = row_blocks;
+    if (M == 1 && env_int("VG_WS_M", 1, 1, 2) == 2 && 2 * R <= 255) {
+      Mw = 2;
+      rbw = (d.W + 2 * R - 1) / (2 * R);
+    }
+    p.row_blocks = rbw;
+    p.z_blocks = z_blocks;
+    p.cta_order = 0;
+    p.tasks = p.n_jchunks * rbw * z_blocks;
+    p.n_molecules = (int)d.n_molecules;
+    if (p.gx_win > 0 && !(p.gx_win < round_up4(Mw * R))) p.gx_win = 0;
+    const int rc = launch_ws(d, L, ws, p, Mw, R, nt, jc, st);
+    if (rc == VG_OK && kernels != nullptr) *kernels += 1;
+    return rc;
+  }
   // staged block per candidate: gy[pad4(jc)] gx[window or pad4(M*R)] gz[pad4(zw*width)]
   p.stage_gx = (jc + 3) & ~3;
   p.stage_gz = p.stage_gx + (p.gx_win > 0 ? p.gx_win : round_up4(M * R));
@@ -2290,6 +2963,15 @@ VG_API int vg_exp_timing_fetch_warps(void* host, size_t bytes) {
 VG_API int vg_exp_timing_fetch(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_vg_ts, bytes < sizeof(g_vg_ts) ? bytes : sizeof(g_vg_ts)) ==
                  cudaSuccess ? VG_OK : VG_ERR_CUDA;
+}
+#endif
+
+#ifdef VG_EXP_WSPROF
+VG_API int vg_exp_wsprof(void* host, int reset) {
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (host != nullptr && cudaMemcpyFromSymbol(host, g_ws_prof, sizeof z) != cudaSuccess) return VG_ERR_CUDA;
+  if (reset && cudaMemcpyToSymbol(g_ws_prof, z, sizeof z) != cudaSuccess) return VG_ERR_CUDA;
+  return VG_OK;
 }
 #endif
 

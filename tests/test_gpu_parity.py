@@ -666,3 +666,32 @@ def test_unaligned_output_pointer_vs_oracle():
         ref, _ = orc.batch(pb.offsets, pb.channels, pb.xyz, geom_of(cfg), workers=orc.host_cores())
         assert_bitwise(out.cpu().numpy(), ref, f"unaligned cfg{k}")
         assert float(buf[0]) == 7.0
+
+
+@pytest.mark.parametrize("env", [{"VG_WS": "1", "VG_WS_NP": "1"},
+                                 {"VG_WS": "1", "VG_WS_NP": "2", "VG_WS_STAGES": "5"},
+                                 {"VG_WS": "1", "VG_WS_NP": "1", "VG_WS_CAP": "8",
+                                  "VG_WS_STAGES": "2"},
+                                 {"VG_WS": "1", "VG_WS_NP": "2", "VG_WS_M": "2"}])
+def test_warp_specialised_k3w_vs_oracle(env, monkeypatch):
+    """The persistent, warp-specialised K3W (producer warps, mbarrier ring,
+    cp.async.bulk staging; opt-in with VG_WS=1) gives the oracle's bits and
+    counters on binned batches: cfg3 clusters, a tiny staging capacity that
+    forces segments, and mixed molecule sizes with an invalid atom."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = synth.CONFIGS[3]
+    _compare_with_oracle(cfg, [0, 5, 17])
+    rng = np.random.default_rng(23)
+    sizes = [1300, 0, 5, 2100, 800]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ch = rng.integers(0, 3, size=off[-1]).astype(np.int32)
+    xyz = rng.normal(6.0, 2.5, size=(off[-1], 3))
+    spec = vg.GridSpec((38, 30, 48), 3, vg.BoundingBox((0, 0, 0), (12, 12, 12)), 0.45)
+    geom = orc.Geometry((38, 30, 48), 3, (0, 0, 0), (12, 12, 12), 0.45)
+    g, st = vg.generate_packed(off, ch, xyz, spec)
+    ref, rs = orc.batch(off, ch, xyz, geom, workers=orc.host_cores())
+    assert_bitwise(g.cpu().numpy(), ref, f"K3W mixed {env}")
+    s = st.cpu().numpy()
+    assert [int(v) for v in s[:, 0]] == [r["voxel_writes"] for r in rs]
+    assert [int(v) for v in s[:, 1]] == [r["nonzero_voxels"] for r in rs]
