@@ -11,7 +11,7 @@
 //     Cody-Waite reduction x = k*ln2 + r with ln2 split hi/lo, a Remez
 //     (5,2) rational approximation of exp(r), then an exact 2^k scaling.
 //     Conformance: all 2^32 float32 inputs bit-identical to np.exp (float32)
-//     on an AVX512_SKX host (tests/test_math_host.py).
+//     on an AVX512_SKX host (tests/test_math_host.py, `pytest --runslow`).
 //   * the Bürmann-series erf of the reference, /root/reference/pkg/src/
 //     voxgrid/kernels.py:43-56 (_erf_core), in its exact fp32 op order.
 //   * the fp64 edge arguments, kernels.py:131-136 / :252-254 (+ periodic

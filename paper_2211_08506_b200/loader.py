@@ -24,6 +24,8 @@ previous consumer-visible event.
 from __future__ import annotations
 
 import ctypes
+import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,7 +34,7 @@ from . import _native
 from .core import GridSpec
 from .gridgen import GridEngine, _require_cuda, check_packed, raise_if_flagged
 
-__all__ = ["GridPipeline", "PipelineResult"]
+__all__ = ["GridPipeline", "PipelineResult", "shared_pipeline", "generate_rows"]
 
 
 @dataclass
@@ -66,6 +68,9 @@ class _Slot:
         self._host = None
         self.out_b = -1                           # batch size `out` was allocated for
         self.ptrs = None                          # (out, ws, ws bytes, stats) pointers
+        self.pinned = None                        # pinned host staging (staging())
+        self.staged = None                        # layout of the last staging() call
+        self._boxes = None
 
 
 class GridPipeline:
@@ -112,14 +117,43 @@ class GridPipeline:
             return t
         return t.to(self.device, dtype).contiguous()
 
-    def submit(self, offsets, channels, xyz, release=None, stats_out=None) -> PipelineResult:
+    def staging(self, B: int, n: int):
+        """Pinned host buffers ``(offsets int64 [B+1], channels int32 [n],
+        xyz fp64 [n, 3])`` (numpy views) for the batch the NEXT ``submit``
+        queues. Fill them and pass them to ``submit``: the copy is then a
+        true asynchronous H2D. Blocks only until that slot's previous copy
+        has read its buffers (``depth`` submissions ago)."""
+        torch = self.torch
+        slot = self.slots[self.k % len(self.slots)]
+        if slot.used:
+            slot.events[0].synchronize()       # ev_copied of the slot's last use
+        need = (B + 1) * 8 + n * 4 + 256 + n * 24
+        if slot.pinned is None or slot.pinned.numel() < need:
+            grow = 2 if slot.pinned is not None else 1
+            slot.pinned = torch.empty(max(need * grow, 1 << 16), dtype=torch.uint8).pin_memory()
+        buf = slot.pinned.numpy()
+        off = buf[:(B + 1) * 8].view(np.int64)
+        x0 = ((B + 1) * 8 + 255) & ~255
+        xyz = buf[x0:x0 + n * 24].view(np.float64).reshape(n, 3)
+        c0 = x0 + n * 24
+        ch = buf[c0:c0 + n * 4].view(np.int32)
+        slot.staged = (slot.pinned, (0, (B + 1) * 8), (c0, n * 4), (x0, n * 24))
+        return off, ch, xyz
+
+    def submit(self, offsets, channels, xyz, release=None, stats_out=None, out=None,
+               mol_origin=None, mol_delta=None, validated=False) -> PipelineResult:
         """Queue one CSR batch (numpy/torch, host or device). Returns at once.
 
         One native call (``vg_submit_f32``) queues the H2D copies (copy
         stream), K1 (tables stream) and K2/K3 (compute stream), ordered by the
         slot's events. ``stats_out``: optional pinned host int64 (B, 2) tensor
         that receives the per-grid stats (D2H on the compute stream, complete
-        at ``ready``)."""
+        at ``ready``). ``out``: a contiguous float32 (B, C, H, W, D) device
+        tensor (e.g. a slice of a larger batch) to write instead of the
+        slot's own buffer; the caller orders its later use after ``ready``.
+        ``mol_origin``/``mol_delta``: per-molecule boxes (device fp64 (B, 3),
+        alive until ``ready``). ``validated``: host inputs were already
+        checked (``check_packed``) by the caller."""
         torch = self.torch
         spec = self.spec
         slot = self.slots[self.k % len(self.slots)]
@@ -170,17 +204,30 @@ class GridPipeline:
             args.h_offsets = args.h_channel = args.h_xyz = None
             host = (off_d, ch_d, xyz_d)
         else:
-            host = (_host_array(offsets, torch.int64), _host_array(channels, torch.int32),
-                    _host_array(xyz, torch.float64))
-            if self.validate:
-                check_packed(host[0].numpy(), host[1].numpy(), host[2].numpy(), spec.channels)
+            staged = slot.staged
+            slot.staged = None
+            if staged is not None and isinstance(offsets, np.ndarray) \
+                    and offsets.ctypes.data == staged[0].data_ptr():
+                # filled staging() buffers: pinned, already in kernel dtypes
+                base = staged[0].data_ptr()
+                h_ptrs = (base, base + staged[2][0], base + staged[3][0])
+                host = (staged[0],)
+                if self.validate and not validated:
+                    check_packed(offsets, channels, xyz, spec.channels)
+            else:
+                host = (_host_array(offsets, torch.int64), _host_array(channels, torch.int32),
+                        _host_array(xyz, torch.float64))
+                if self.validate and not validated:
+                    check_packed(host[0].numpy(), host[1].numpy(), host[2].numpy(),
+                                 spec.channels)
+                h_ptrs = tuple(h.data_ptr() for h in host)
             slot.off = self._ensure(slot.off, B + 1, torch.int64)
             slot.ch = self._ensure(slot.ch, n, torch.int32)
             slot.xyz = self._ensure(slot.xyz, 3 * n, torch.float64)
             off_d, ch_d, xyz_d = slot.off, slot.ch, slot.xyz
-            args.h_offsets = host[0].data_ptr()
-            args.h_channel = host[1].data_ptr() if n else None
-            args.h_xyz = host[2].data_ptr() if n else None
+            args.h_offsets = h_ptrs[0]
+            args.h_channel = h_ptrs[1] if n else None
+            args.h_xyz = h_ptrs[2] if n else None
 
         desc = slot.desc
         if desc is None:
@@ -191,23 +238,43 @@ class GridPipeline:
         desc.offsets = off_d.data_ptr()
         desc.channel = ch_d.data_ptr() if n else None
         desc.xyz = xyz_d.data_ptr() if n else None
+        if (mol_origin is None) != (mol_delta is None):
+            raise ValueError("mol_origin and mol_delta go together")
+        for t in (mol_origin, mol_delta):
+            if t is not None and (not t.is_cuda or t.dtype != torch.float64
+                                  or tuple(t.shape) != (B, 3) or not t.is_contiguous()):
+                raise ValueError("per-molecule boxes must be contiguous fp64 (B, 3) device "
+                                 "tensors")
+        desc.mol_origin = mol_origin.data_ptr() if mol_origin is not None else None
+        desc.mol_delta = mol_delta.data_ptr() if mol_delta is not None else None
         if slot.out_b != B:
-            slot.out = torch.empty((B, spec.channels, H, W, D), dtype=torch.float32,
-                                   device=self.device)
             slot.stats = torch.empty((B, 2), dtype=torch.int64, device=self.device)
+            slot.out = None
             slot.out_b = B
             slot.ptrs = None
+        if out is not None:
+            if (tuple(out.shape) != (B, spec.channels, H, W, D) or out.dtype != torch.float32
+                    or not out.is_contiguous() or out.device != self.device):
+                raise ValueError("out must be a contiguous float32 (B, C, H, W, D) tensor on "
+                                 "the pipeline's device")
+            grids = out
+        else:
+            if slot.out is None:
+                slot.out = torch.empty((B, spec.channels, H, W, D), dtype=torch.float32,
+                                       device=self.device)
+                slot.ptrs = None
+            grids = slot.out
         args.h_stats = stats_out.data_ptr() if stats_out is not None else None
         if slot.ws is None:
             slot.ws = torch.empty(1 << 20, dtype=torch.uint8, device=self.device)
             slot.ptrs = None
-        if slot.ptrs is None:
-            slot.ptrs = (slot.out.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
+        if slot.ptrs is None or slot.ptrs[0] != grids.data_ptr():
+            slot.ptrs = (grids.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
                          slot.stats.data_ptr())
         rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         if rc == _native.VG_ERR_WORKSPACE and slot.ws_needed.value > slot.ws.numel():
             slot.ws = torch.empty(slot.ws_needed.value, dtype=torch.uint8, device=self.device)
-            slot.ptrs = (slot.out.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
+            slot.ptrs = (grids.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
                          slot.stats.data_ptr())
             rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         _native.check(rc, "vg_submit_f32")
@@ -216,7 +283,8 @@ class GridPipeline:
         ready = slot.events[3] if slot.read_back else slot.events[2]
         # keep the inputs alive until the copy / kernels have read them
         slot._host = host
-        return PipelineResult(slot.out, slot.stats, ready, (self.k - 1) % len(self.slots))
+        slot._boxes = (mol_origin, mol_delta)
+        return PipelineResult(grids, slot.stats, ready, (self.k - 1) % len(self.slots))
 
     def begin(self, event):
         """Make every stage wait for ``event`` (e.g. the start of a timed region)."""
@@ -252,3 +320,107 @@ def pinned_csr(offsets, channels, xyz):
     return (torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).pin_memory(),
             torch.from_numpy(np.ascontiguousarray(channels, dtype=np.int32)).pin_memory(),
             torch.from_numpy(np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1)).pin_memory())
+
+
+# ---------------------------------------------------------------------------
+# the drop-in APIs on the pipeline (GaussianVoxelizer.transform)
+# ---------------------------------------------------------------------------
+_SHARED: OrderedDict = OrderedDict()
+_SHARED_LOCK = threading.Lock()
+_SHARED_MAX = 8
+
+
+def shared_pipeline(spec: GridSpec, device=None, mode: str = "sparse", threshold=None):
+    """The process-wide pipeline of (device, spec, mode, threshold), with the
+    lock a caller holds while it queues one call's chunks (LRU of 8)."""
+    dev = _require_cuda(device)
+    key = (dev.index, spec, mode, threshold)
+    with _SHARED_LOCK:
+        hit = _SHARED.get(key)
+        if hit is None:
+            hit = (GridPipeline(spec, dev, mode=mode, threshold=threshold, depth=3),
+                   threading.Lock())
+            _SHARED[key] = hit
+            while len(_SHARED) > _SHARED_MAX:
+                _SHARED.popitem(last=False)
+        _SHARED.move_to_end(key)
+        return hit
+
+
+def _rows_chunk(part, C: int):
+    """(counts, rows) of a chunk of (m, 4) point arrays, validated in one pass;
+    None when any array needs the per-sample path (shape, values or channel
+    range: that path raises the reference's error for the first offender)."""
+    try:
+        rows = np.concatenate(part, axis=0)
+    except (ValueError, TypeError):
+        return None
+    if rows.ndim != 2 or rows.shape[1] != 4:
+        return None
+    if rows.dtype != np.float64:
+        try:
+            rows = rows.astype(np.float64)
+        except (ValueError, TypeError):
+            return None
+    counts = np.fromiter(map(len, part), dtype=np.int64, count=len(part))
+    if rows.shape[0]:
+        ch = rows[:, 0]
+        if not (np.isfinite(rows.sum()) and ch.min() >= 0 and ch.max() < C
+                and np.array_equal(ch, np.floor(ch))):
+            return None
+    return counts, rows
+
+
+def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", threshold=None,
+                  first: int = 64, max_chunk: int = 256):
+    """Grids of a batch of (m_i, 4) host arrays of (channel, x, y, z) rows into
+    one CUDA float32 tensor (B, C, H, W, D) — the fast path of
+    ``GaussianVoxelizer.transform`` (estimator.py:134-151) for a shared box.
+
+    The batch is cut into chunks (``first`` molecules, doubling up to
+    ``max_chunk``): chunk k+1 is validated and packed straight into pinned
+    staging while the device copies, tables and writes chunk k into its slice
+    of the output, so the host work hides behind the HBM-bound slab kernel.
+    The caller's current stream is ordered after the last chunk on return.
+    Returns None (after ordering any queued chunk) when a sample needs the
+    per-sample path, which then raises the reference's error."""
+    torch = _torch()
+    dev = _require_cuda(device)
+    H, W, D = spec.shape
+    B = len(X)
+    out = torch.empty((B, spec.channels, H, W, D), dtype=torch.float32, device=dev)
+    if B == 0:
+        return out
+    pipe, lock = shared_pipeline(spec, dev, mode, threshold)
+    cur = torch.cuda.current_stream(dev)
+    last = None
+    with lock:
+        start = torch.cuda.Event()
+        start.record(cur)          # `out` was allocated on the caller's stream
+        pipe.begin(start)
+        try:
+            b, size = 0, max(1, first)
+            while b < B:
+                e = min(B, b + size)
+                part = X[b:e]
+                got = _rows_chunk(part, spec.channels)
+                if got is None:
+                    return None
+                counts, rows = got
+                off, ch, xyz = pipe.staging(e - b, rows.shape[0])
+                off[0] = 0
+                np.cumsum(counts, out=off[1:])
+                ch[:] = rows[:, 0]
+                xyz[:] = rows[:, 1:4]
+                last = pipe.submit(off, ch, xyz, out=out[b:e], validated=True)
+                b, size = e, min(2 * size, max(max_chunk, 1))
+        finally:
+            if last is not None:
+                cur.wait_event(last.ready)
+    return out
+
+
+def _torch():
+    import torch
+
+    return torch

@@ -600,6 +600,47 @@ def test_estimator_packed_fast_path_equals_per_sample_path():
         est.transform(bad)
 
 
+def test_transform_chunked_pipeline_equals_single_launch():
+    """transform's chunked, pipelined path (loader.generate_rows: pinned
+    staging, one GridPipeline submit per chunk into slices of one output)
+    gives the single-launch bits for every chunk schedule, empty samples
+    included, and the result is usable on the caller's stream without a
+    sync; a bad sample in a LATE chunk still raises the reference's error."""
+    from paper_2211_08506_b200.loader import generate_rows
+
+    cfg = synth.CONFIGS[0]
+    pb = synth.packed_batch(cfg, range(37))
+    X = [np.column_stack([pb.channels[a:b].astype(np.float64), pb.xyz.reshape(-1, 3)[a:b]])
+         for a, b in zip(pb.offsets[:-1], pb.offsets[1:])]
+    X[5] = np.zeros((0, 4))
+    X[36] = np.zeros((0, 4))
+    spec = spec_of(cfg)
+    offs = np.concatenate([[0], np.cumsum([len(x) for x in X])])
+    rows = np.concatenate(X)
+    ref, _ = vg.generate_packed(offs, rows[:, 0].astype(np.int32), rows[:, 1:4], spec)
+    ref = ref.cpu().numpy()
+    for first, cap in ((1, 1), (1, 4), (3, 7), (64, 256), (37, 37)):
+        got = generate_rows(X, spec, first=first, max_chunk=cap)
+        # consumed on the current stream with no explicit synchronisation
+        digest = got.view(torch.int32).sum(dim=(1, 2, 3, 4), dtype=torch.int64).cpu().numpy()
+        assert np.array_equal(digest, ref.view(np.int32).astype(np.int64).sum(axis=(1, 2, 3, 4)))
+        assert_bitwise(got.cpu().numpy(), ref, f"chunks {first}/{cap}")
+    est = vg.GaussianVoxelizer(grid_size=cfg.shape, sigma=cfg.sigma, n_channels=cfg.channels,
+                               box=(cfg.box_origin, cfg.box_extents)).fit(X)
+    assert_bitwise(est.transform(X).cpu().numpy(), ref, "transform")
+    assert generate_rows([], spec).shape == (0, 5, 32, 32, 32)
+    for late in (30, 36):
+        for bad_row in ([[7.0, 1.0, 1.0, 1.0]], [[1.0, np.nan, 1.0, 1.0]], [[0.5, 1, 1, 1]],
+                        [[1.0, 1.0, 1.0]]):
+            bad = list(X)
+            bad[late] = np.array(bad_row)
+            assert generate_rows(bad, spec, first=4, max_chunk=8) is None
+            with pytest.raises(ValueError):
+                est.transform(bad)
+    # the pipeline is intact after the failures
+    assert_bitwise(est.transform(X).cpu().numpy(), ref, "transform after failures")
+
+
 def test_pipeline_edge_batches():
     """GridPipeline over an empty batch, a batch of empty molecules and a
     periodic spec, reusing slots: every result equals the serial path and the
