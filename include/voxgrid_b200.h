@@ -111,7 +111,10 @@ int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
  * Events are caller-created cudaEvent_t (passed as void*); ev_wait may be
  * NULL and may be the same event as ev_done (the wait uses its previous
  * record). Returns at once: no host synchronisation. Host buffers must stay
- * valid (pinned for asynchronous copies) until ev_copied / ev_done.
+ * valid (pinned for asynchronous copies) until ev_copied / ev_done. When the
+ * three host arrays lie in one block with the same relative offsets as their
+ * device destinations (offsets first, xyz and channel not overlapping), the
+ * copy stage is a single H2D of that span.
  * VG_ERR_WORKSPACE sets *ws_needed (if non-NULL) to the bytes required. */
 typedef struct vg_submit_args {
   const void* h_offsets;   /* host [B+1] int64, or NULL: desc->offsets already filled   */

@@ -184,6 +184,51 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     return LIB_PATH
 
 
+def _pack_path() -> Path:
+    import sysconfig
+
+    return PKG_DIR / ("_vgpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pack(force: bool = False) -> Path:
+    """Compile csrc/vg_pack.cpp (CPython extension ``_vgpack``: the host
+    packer of the drop-in APIs) in-tree with g++."""
+    import sysconfig
+
+    src = CSRC / "vg_pack.cpp"
+    out = _pack_path()
+    if not force and out.exists() and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    tmp = out.with_suffix(".so.tmp")
+    import numpy
+
+    cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-shared", "-fPIC",
+           "-fvisibility=hidden", f"-I{sysconfig.get_paths()['include']}",
+           f"-I{numpy.get_include()}", "-o", str(tmp), str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
+_pack = None
+
+
+def pack():
+    """The ``_vgpack`` host packer module (built on first use if missing)."""
+    global _pack
+    if _pack is None:
+        import importlib.util
+
+        path = build_pack()
+        spec = importlib.util.spec_from_file_location("_vgpack", path)
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        _pack = mod
+    return _pack
+
+
 def lib():
     """The loaded library (raises NativeUnavailable if it is not built)."""
     global _lib

@@ -2867,15 +2867,34 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   // and K3 follow it through ev_copied / ev_tabled, so they are ordered
   // after that consumer too
   if (ev_wait != nullptr) ok(cudaStreamWaitEvent(cs, ev_wait, 0));
-  if (a->h_offsets != nullptr && B > 0)
-    ok(cudaMemcpyAsync(const_cast<int64_t*>(desc->offsets), a->h_offsets, (size_t)(B + 1) * 8,
-                       cudaMemcpyHostToDevice, cs));
-  if (n > 0 && a->h_channel != nullptr)
-    ok(cudaMemcpyAsync(const_cast<int32_t*>(desc->channel), a->h_channel, (size_t)n * 4,
-                       cudaMemcpyHostToDevice, cs));
-  if (n > 0 && a->h_xyz != nullptr)
-    ok(cudaMemcpyAsync(const_cast<double*>(desc->xyz), a->h_xyz, (size_t)n * 24,
-                       cudaMemcpyHostToDevice, cs));
+  // One H2D when the three host arrays sit in one block with the same
+  // relative layout as their device destinations (GridPipeline.staging):
+  // offsets first, then xyz and channels in either order, no overlap.
+  const char* ho = static_cast<const char*>(a->h_offsets);
+  const char* hx = static_cast<const char*>(a->h_xyz);
+  const char* hc = static_cast<const char*>(a->h_channel);
+  const char* dof = reinterpret_cast<const char*>(desc->offsets);
+  const char* dx = reinterpret_cast<const char*>(desc->xyz);
+  const char* dc = reinterpret_cast<const char*>(desc->channel);
+  const int64_t ob = (B + 1) * 8, xb = n * 24, cb = n * 4;
+  const bool one_block = B > 0 && n > 0 && ho != nullptr && hx != nullptr && hc != nullptr &&
+                         hx - ho == dx - dof && hc - ho == dc - dof && hx - ho >= ob &&
+                         hc - ho >= ob && (hc - hx >= xb || hx - hc >= cb);
+  if (one_block) {
+    const int64_t xe = (hx - ho) + xb, ce = (hc - ho) + cb;
+    const int64_t span = xe > ce ? xe : ce;
+    ok(cudaMemcpyAsync(const_cast<char*>(dof), ho, (size_t)span, cudaMemcpyHostToDevice, cs));
+  } else {
+    if (a->h_offsets != nullptr && B > 0)
+      ok(cudaMemcpyAsync(const_cast<int64_t*>(desc->offsets), a->h_offsets, (size_t)ob,
+                         cudaMemcpyHostToDevice, cs));
+    if (n > 0 && a->h_channel != nullptr)
+      ok(cudaMemcpyAsync(const_cast<int32_t*>(desc->channel), a->h_channel, (size_t)cb,
+                         cudaMemcpyHostToDevice, cs));
+    if (n > 0 && a->h_xyz != nullptr)
+      ok(cudaMemcpyAsync(const_cast<double*>(desc->xyz), a->h_xyz, (size_t)xb,
+                         cudaMemcpyHostToDevice, cs));
+  }
   ok(cudaEventRecord(ev_copied, cs));
   ok(cudaStreamWaitEvent(ts, ev_copied, 0));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (copy stage): %s", cudaGetErrorString(e));

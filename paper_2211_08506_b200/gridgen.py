@@ -49,6 +49,10 @@ __all__ = [
 
 _MODES = ("dense", "sparse")
 
+# generate_batch runs batches larger than this through the chunked pipeline
+# (without an explicit stream / engine); smaller ones in one launch pair
+PIPELINE_MIN_BATCH = 128
+
 
 @dataclass
 class GenStats:
@@ -117,7 +121,7 @@ class GridEngine:
     def describe(self, offsets, channels, xyz, spec: GridSpec, *, mol_origin=None,
                  mol_delta=None, mode="sparse", threshold=None) -> _native.VgBatchDesc:
         """Fill the C descriptor (device tensors already on self.device)."""
-        d = _native.VgBatchDesc()
+        d = self.describe_spec(spec, mode=mode, threshold=threshold)
         d.n_molecules = int(offsets.numel() - 1)
         d.n_atoms = int(channels.numel())
         d.offsets = offsets.data_ptr()
@@ -125,6 +129,12 @@ class GridEngine:
         d.channel = channels.data_ptr() if d.n_atoms else None
         d.mol_origin = mol_origin.data_ptr() if mol_origin is not None else None
         d.mol_delta = mol_delta.data_ptr() if mol_delta is not None else None
+        return d
+
+    @staticmethod
+    def describe_spec(spec: GridSpec, *, mode="sparse", threshold=None) -> _native.VgBatchDesc:
+        """A descriptor with the geometry of ``spec`` (no batch pointers yet)."""
+        d = _native.VgBatchDesc()
         (_, ox, dx), (_, oy, dy), (_, oz, dz) = spec.axis_params()
         d.origin[:] = (ox, oy, oz)
         d.delta[:] = (dx, dy, dz)
@@ -497,10 +507,22 @@ def generate_batch(point_sets: Sequence, spec: GridSpec, spec_policy: str = "fix
     specs = [spec] * len(point_sets)
     if spec_policy == "per-molecule-bbox":
         mol_origin, mol_delta, specs = _bbox_policy(point_sets, spec, padding_sigmas, errors)
-    offsets, channels, xyz, counts = pack_particle_sets(point_sets, spec, errors)
-    tensor, stats = generate_packed(offsets, channels, xyz, spec, mol_origin=mol_origin,
-                                    mol_delta=mol_delta, mode=mode, threshold=threshold,
-                                    device=device, stream=stream, engine=engine)
+    if stream is None and engine is None and len(point_sets) > PIPELINE_MIN_BATCH:
+        # large batch: chunks gathered into pinned staging while the device
+        # works on the previous chunk (loader.generate_sets)
+        from .loader import generate_sets
+
+        counts = np.array([len(ps) for ps in point_sets], dtype=np.int64).reshape(-1)
+        for b in errors:
+            counts[b] = 0
+        tensor, stats = generate_sets(point_sets, spec, counts, mol_origin=mol_origin,
+                                      mol_delta=mol_delta, device=device, mode=mode,
+                                      threshold=threshold)
+    else:
+        offsets, channels, xyz, counts = pack_particle_sets(point_sets, spec, errors)
+        tensor, stats = generate_packed(offsets, channels, xyz, spec, mol_origin=mol_origin,
+                                        mol_delta=mol_delta, mode=mode, threshold=threshold,
+                                        device=device, stream=stream, engine=engine)
     images = 3 if spec.periodic is not None else 1
     return BatchResult(tensor, specs, errors, stats, counts, mode, images,
                        time.perf_counter() - start)

@@ -34,7 +34,7 @@ from . import _native
 from .core import GridSpec
 from .gridgen import GridEngine, _require_cuda, check_packed, raise_if_flagged
 
-__all__ = ["GridPipeline", "PipelineResult", "shared_pipeline", "generate_rows"]
+__all__ = ["GridPipeline", "PipelineResult", "shared_pipeline", "generate_rows", "generate_sets"]
 
 
 @dataclass
@@ -69,6 +69,8 @@ class _Slot:
         self.out_b = -1                           # batch size `out` was allocated for
         self.ptrs = None                          # (out, ws, ws bytes, stats) pointers
         self.pinned = None                        # pinned host staging (staging())
+        self.pinned_np = None
+        self.blk = None                           # device mirror of the staging block
         self.staged = None                        # layout of the last staging() call
         self._boxes = None
 
@@ -102,6 +104,8 @@ class GridPipeline:
         self.slots = [_Slot() for _ in range(depth)]
         self.k = 0
         self.launches = 0
+        self.atoms_per_mol = 32.0      # staging estimate of generate_rows
+        self.start_event = torch.cuda.Event()   # generate_rows / generate_sets ordering
 
     # -- buffers ---------------------------------------------------------------
     def _ensure(self, t, n, dtype, shape=None):
@@ -131,17 +135,19 @@ class GridPipeline:
         if slot.pinned is None or slot.pinned.numel() < need:
             grow = 2 if slot.pinned is not None else 1
             slot.pinned = torch.empty(max(need * grow, 1 << 16), dtype=torch.uint8).pin_memory()
-        buf = slot.pinned.numpy()
-        off = buf[:(B + 1) * 8].view(np.int64)
+            slot.pinned_np = slot.pinned.numpy()
+        buf = slot.pinned_np
         x0 = ((B + 1) * 8 + 255) & ~255
-        xyz = buf[x0:x0 + n * 24].view(np.float64).reshape(n, 3)
         c0 = x0 + n * 24
+        off = buf[:(B + 1) * 8].view(np.int64)
+        xyz = buf[x0:c0].view(np.float64).reshape(n, 3)
         ch = buf[c0:c0 + n * 4].view(np.int32)
-        slot.staged = (slot.pinned, (0, (B + 1) * 8), (c0, n * 4), (x0, n * 24))
+        # (buffer, its address, channel offset, xyz offset)
+        slot.staged = (slot.pinned, slot.pinned.data_ptr(), c0, x0)
         return off, ch, xyz
 
     def submit(self, offsets, channels, xyz, release=None, stats_out=None, out=None,
-               mol_origin=None, mol_delta=None, validated=False) -> PipelineResult:
+               mol_origin=None, mol_delta=None, validated=False, stats=None) -> PipelineResult:
         """Queue one CSR batch (numpy/torch, host or device). Returns at once.
 
         One native call (``vg_submit_f32``) queues the H2D copies (copy
@@ -151,6 +157,7 @@ class GridPipeline:
         at ``ready``). ``out``: a contiguous float32 (B, C, H, W, D) device
         tensor (e.g. a slice of a larger batch) to write instead of the
         slot's own buffer; the caller orders its later use after ``ready``.
+        ``stats``: likewise a device int64 (B, 2) tensor for the counters.
         ``mol_origin``/``mol_delta``: per-molecule boxes (device fp64 (B, 3),
         alive until ``ready``). ``validated``: host inputs were already
         checked (``check_packed``) by the caller."""
@@ -203,17 +210,25 @@ class GridPipeline:
                     t.record_stream(self.compute_stream)
             args.h_offsets = args.h_channel = args.h_xyz = None
             host = (off_d, ch_d, xyz_d)
+            d_ptrs = (off_d.data_ptr(), ch_d.data_ptr(), xyz_d.data_ptr())
         else:
             staged = slot.staged
             slot.staged = None
             if staged is not None and isinstance(offsets, np.ndarray) \
-                    and offsets.ctypes.data == staged[0].data_ptr():
-                # filled staging() buffers: pinned, already in kernel dtypes
-                base = staged[0].data_ptr()
-                h_ptrs = (base, base + staged[2][0], base + staged[3][0])
+                    and offsets.ctypes.data == staged[1]:
+                # filled staging() buffers: pinned, in kernel dtypes, one block
+                # whose layout the device block mirrors (a single H2D)
+                base, c0, x0 = staged[1], staged[2], staged[3]
+                h_ptrs = (base, base + c0, base + x0)
                 host = (staged[0],)
                 if self.validate and not validated:
                     check_packed(offsets, channels, xyz, spec.channels)
+                span = c0 + 4 * n
+                if slot.blk is None or slot.blk.numel() < span:
+                    slot.blk = torch.empty(max(span, 2 * staged[0].numel()), dtype=torch.uint8,
+                                           device=self.device)
+                dbase = slot.blk.data_ptr()
+                d_ptrs = (dbase, dbase + c0, dbase + x0)
             else:
                 host = (_host_array(offsets, torch.int64), _host_array(channels, torch.int32),
                         _host_array(xyz, torch.float64))
@@ -221,23 +236,23 @@ class GridPipeline:
                     check_packed(host[0].numpy(), host[1].numpy(), host[2].numpy(),
                                  spec.channels)
                 h_ptrs = tuple(h.data_ptr() for h in host)
-            slot.off = self._ensure(slot.off, B + 1, torch.int64)
-            slot.ch = self._ensure(slot.ch, n, torch.int32)
-            slot.xyz = self._ensure(slot.xyz, 3 * n, torch.float64)
-            off_d, ch_d, xyz_d = slot.off, slot.ch, slot.xyz
+                slot.off = self._ensure(slot.off, B + 1, torch.int64)
+                slot.ch = self._ensure(slot.ch, n, torch.int32)
+                slot.xyz = self._ensure(slot.xyz, 3 * n, torch.float64)
+                d_ptrs = (slot.off.data_ptr(), slot.ch.data_ptr(), slot.xyz.data_ptr())
             args.h_offsets = h_ptrs[0]
             args.h_channel = h_ptrs[1] if n else None
             args.h_xyz = h_ptrs[2] if n else None
 
         desc = slot.desc
         if desc is None:
-            desc = slot.desc = self.engine.describe(off_d, ch_d, xyz_d, spec,
-                                                    mode=self.mode, threshold=self.threshold)
+            desc = slot.desc = self.engine.describe_spec(spec, mode=self.mode,
+                                                         threshold=self.threshold)
         desc.n_molecules = B
         desc.n_atoms = n
-        desc.offsets = off_d.data_ptr()
-        desc.channel = ch_d.data_ptr() if n else None
-        desc.xyz = xyz_d.data_ptr() if n else None
+        desc.offsets = d_ptrs[0]
+        desc.channel = d_ptrs[1] if n else None
+        desc.xyz = d_ptrs[2] if n else None
         if (mol_origin is None) != (mol_delta is None):
             raise ValueError("mol_origin and mol_delta go together")
         for t in (mol_origin, mol_delta):
@@ -268,14 +283,23 @@ class GridPipeline:
         if slot.ws is None:
             slot.ws = torch.empty(1 << 20, dtype=torch.uint8, device=self.device)
             slot.ptrs = None
-        if slot.ptrs is None or slot.ptrs[0] != grids.data_ptr():
+        if stats is not None:
+            if (tuple(stats.shape) != (B, 2) or stats.dtype != torch.int64
+                    or not stats.is_contiguous() or stats.device != self.device):
+                raise ValueError("stats must be a contiguous int64 (B, 2) tensor on the "
+                                 "pipeline's device")
+            counters = stats
+        else:
+            counters = slot.stats
+        if (slot.ptrs is None or slot.ptrs[0] != grids.data_ptr()
+                or slot.ptrs[3] != counters.data_ptr()):
             slot.ptrs = (grids.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
-                         slot.stats.data_ptr())
+                         counters.data_ptr())
         rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         if rc == _native.VG_ERR_WORKSPACE and slot.ws_needed.value > slot.ws.numel():
             slot.ws = torch.empty(slot.ws_needed.value, dtype=torch.uint8, device=self.device)
             slot.ptrs = (grids.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
-                         slot.stats.data_ptr())
+                         counters.data_ptr())
             rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         _native.check(rc, "vg_submit_f32")
         self.launches += slot.kernels.value   # K1, K2 (binned batches), K3
@@ -284,7 +308,7 @@ class GridPipeline:
         # keep the inputs alive until the copy / kernels have read them
         slot._host = host
         slot._boxes = (mol_origin, mol_delta)
-        return PipelineResult(grids, slot.stats, ready, (self.k - 1) % len(self.slots))
+        return PipelineResult(grids, counters, ready, (self.k - 1) % len(self.slots))
 
     def begin(self, event):
         """Make every stage wait for ``event`` (e.g. the start of a timed region)."""
@@ -372,15 +396,17 @@ def _rows_chunk(part, C: int):
 
 
 def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", threshold=None,
-                  first: int = 64, max_chunk: int = 256):
+                  first: int = 128, max_chunk: int = 1 << 30):
     """Grids of a batch of (m_i, 4) host arrays of (channel, x, y, z) rows into
     one CUDA float32 tensor (B, C, H, W, D) — the fast path of
     ``GaussianVoxelizer.transform`` (estimator.py:134-151) for a shared box.
 
-    The batch is cut into chunks (``first`` molecules, doubling up to
-    ``max_chunk``): chunk k+1 is validated and packed straight into pinned
-    staging while the device copies, tables and writes chunk k into its slice
-    of the output, so the host work hides behind the HBM-bound slab kernel.
+    The batch is cut into chunks (``first`` molecules, then doubling up to
+    ``max_chunk``; by default a short first chunk and the rest): each chunk is
+    validated and packed by the native packer straight into pinned staging
+    and written by the device into its slice of the output, so the device
+    starts after a short first chunk and the later chunks' copies and tables
+    (K1) overlap the HBM-bound slab kernel (K3) of the earlier ones.
     The caller's current stream is ordered after the last chunk on return.
     Returns None (after ordering any queued chunk) when a sample needs the
     per-sample path, which then raises the reference's error."""
@@ -392,32 +418,113 @@ def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", thres
     if B == 0:
         return out
     pipe, lock = shared_pipeline(spec, dev, mode, threshold)
+    pk = _native.pack()
+    if not isinstance(X, (list, tuple)):
+        X = list(X)
     cur = torch.cuda.current_stream(dev)
     last = None
     with lock:
-        start = torch.cuda.Event()
-        start.record(cur)          # `out` was allocated on the caller's stream
-        pipe.begin(start)
+        # `out` was allocated on the caller's stream: the copy stage (hence
+        # K1 and K3, which follow it) is ordered after the caller's work
+        pipe.start_event.record(cur)
+        pipe.copy_stream.wait_event(pipe.start_event)
         try:
             b, size = 0, max(1, first)
             while b < B:
                 e = min(B, b + size)
-                part = X[b:e]
-                got = _rows_chunk(part, spec.channels)
-                if got is None:
-                    return None
-                counts, rows = got
-                off, ch, xyz = pipe.staging(e - b, rows.shape[0])
-                off[0] = 0
-                np.cumsum(counts, out=off[1:])
-                ch[:] = rows[:, 0]
-                xyz[:] = rows[:, 1:4]
+                # float64 (m, 4) arrays: one native pass validates and writes
+                # the CSR arrays into the pinned staging (sized by a running
+                # atoms-per-molecule estimate; repacked once if it was short)
+                guess = int((e - b) * pipe.atoms_per_mol * 1.25) + 64
+                off, ch, xyz = pipe.staging(e - b, guess)
+                n = pk.rows_pack(X, b, e, spec.channels, off.ctypes.data, ch.ctypes.data,
+                                 xyz.ctypes.data, guess)
+                if n < -1:
+                    off, ch, xyz = pipe.staging(e - b, -n - 2)
+                    n = pk.rows_pack(X, b, e, spec.channels, off.ctypes.data, ch.ctypes.data,
+                                     xyz.ctypes.data, -n - 2)
+                if n >= 0:
+                    pipe.atoms_per_mol = max(1.0, n / (e - b))
+                    ch, xyz = ch[:n], xyz[:n]
+                elif pk.rows_count(X, b, e) >= 0:
+                    return None      # well-formed arrays with invalid values
+                else:
+                    got = _rows_chunk(X[b:e], spec.channels)
+                    if got is None:
+                        return None
+                    counts, rows = got
+                    off, ch, xyz = pipe.staging(e - b, rows.shape[0])
+                    off[0] = 0
+                    np.cumsum(counts, out=off[1:])
+                    ch[:] = rows[:, 0]
+                    xyz[:] = rows[:, 1:4]
                 last = pipe.submit(off, ch, xyz, out=out[b:e], validated=True)
                 b, size = e, min(2 * size, max(max_chunk, 1))
         finally:
             if last is not None:
                 cur.wait_event(last.ready)
     return out
+
+
+def generate_sets(sets, spec: GridSpec, counts, *, mol_origin=None, mol_delta=None, device=None,
+                  mode: str = "sparse", threshold=None, first: int = 64, max_chunk: int = 256):
+    """``generate_batch``'s device work (gridgen.py:173-221) through the shared
+    pipeline: ``(grids (B, C, H, W, D), stats (B, 2))`` CUDA tensors for
+    validated ParticleSets, molecule b contributing ``counts[b]`` atoms (0 for
+    a molecule with a recorded error: its slot stays all zero). Per-molecule
+    boxes (host fp64 (B, 3) origin / voxel sizes) are uploaded once and sliced
+    per chunk. Chunks of atoms are gathered straight into pinned staging
+    (one np.concatenate per array) while the device works on the previous
+    chunk; the caller's stream is ordered after the last chunk."""
+    torch = _torch()
+    dev = _require_cuda(device)
+    H, W, D = spec.shape
+    B = len(sets)
+    out = torch.empty((B, spec.channels, H, W, D), dtype=torch.float32, device=dev)
+    stats = torch.empty((B, 2), dtype=torch.int64, device=dev)
+    if B == 0:
+        return out, stats
+    boxes = None
+    if mol_origin is not None:
+        boxes = (torch.from_numpy(np.ascontiguousarray(mol_origin, dtype=np.float64)).to(dev),
+                 torch.from_numpy(np.ascontiguousarray(mol_delta, dtype=np.float64)).to(dev))
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    pipe, lock = shared_pipeline(spec, dev, mode, threshold)
+    pk = _native.pack()
+    if not isinstance(sets, (list, tuple)):
+        sets = list(sets)
+    cur = torch.cuda.current_stream(dev)
+    last = None
+    with lock:
+        pipe.start_event.record(cur)   # outputs and boxes were made on the caller's stream
+        pipe.copy_stream.wait_event(pipe.start_event)
+        try:
+            b, size = 0, max(1, first)
+            while b < B:
+                e = min(B, b + size)
+                cnt = counts[b:e]
+                n = int(cnt.sum())
+                off, ch, xyz = pipe.staging(e - b, n)
+                if pk.sets_pack(sets, b, e, counts.ctypes.data, off.ctypes.data,
+                                ch.ctypes.data, xyz.ctypes.data, n) != 0:
+                    # arrays the native packer does not take (non-contiguous)
+                    off[0] = 0
+                    np.cumsum(cnt, out=off[1:])
+                    keep = [sets[i] for i in range(b, e) if counts[i]]
+                    if keep:
+                        np.concatenate([ps.channels for ps in keep], out=ch, casting="unsafe")
+                        np.concatenate([np.asarray(ps.positions).reshape(-1, 3) for ps in keep],
+                                       axis=0, out=xyz)
+                mo = md = None
+                if boxes is not None:
+                    mo, md = boxes[0][b:e], boxes[1][b:e]
+                last = pipe.submit(off, ch, xyz, out=out[b:e], stats=stats[b:e],
+                                   mol_origin=mo, mol_delta=md, validated=True)
+                b, size = e, min(2 * size, max(max_chunk, 1))
+        finally:
+            if last is not None:
+                cur.wait_event(last.ready)
+    return out, stats
 
 
 def _torch():

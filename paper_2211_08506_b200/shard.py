@@ -11,7 +11,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["BYTES_PER_ATOM", "molecule_costs", "plan_shards", "shard_range"]
+__all__ = ["BYTES_PER_ATOM", "molecule_costs", "plan_shards", "shard_range", "rank_world",
+           "rank_shard"]
 
 
 # K3 cost of one atom in output-byte equivalents, from per-CTA timing of
@@ -58,3 +59,33 @@ def shard_range(n_molecules: int, rank: int, world_size: int, costs=None) -> ran
         costs = np.ones(n_molecules)
     start, stop = plan_shards(costs, world_size)[rank]
     return range(start, stop)
+
+
+def rank_world(group=None) -> tuple:
+    """``(rank, world_size)`` of this process: from torch.distributed when it
+    is initialised (``group`` optional), else from the launcher's RANK /
+    WORLD_SIZE environment (torchrun), else ``(0, 1)``."""
+    import os
+
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_rank(group), dist.get_world_size(group)
+    except ImportError:  # pragma: no cover - torch is in the image
+        pass
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def rank_shard(n_molecules: int, atom_counts=None, grid_bytes: int = 0, group=None) -> range:
+    """This process's contiguous molecule range of a batch sharded over the
+    job's ranks (one process per GPU, no collective: reference
+    gridgen.py:206-219 fans molecules out the same way inside one process).
+    With ``atom_counts`` and ``grid_bytes`` the cut balances the estimated
+    K3 cost (grid bytes + BYTES_PER_ATOM x atoms) instead of the counts;
+    every rank computes the same plan."""
+    rank, world = rank_world(group)
+    costs = None
+    if atom_counts is not None:
+        costs = molecule_costs(atom_counts, grid_bytes, BYTES_PER_ATOM)
+    return shard_range(n_molecules, rank, world, costs)

@@ -214,8 +214,11 @@ def test_cfg1_full_vs_oracle():
         _compare_with_oracle(cfg, range(start, start + 256))
 
 
-def test_cfg2_strided_sample_vs_oracle():
-    _compare_with_oracle(synth.CONFIGS[2], range(7, 65536, 97))
+def test_cfg2_full_vs_oracle():
+    # all 65,536 grids (2.1 G voxels), in chunks of 4096 molecules
+    cfg = synth.CONFIGS[2]
+    for start in range(0, cfg.n_molecules, 4096):
+        _compare_with_oracle(cfg, range(start, start + 4096))
 
 
 def test_cfg3_full_vs_oracle():
@@ -639,6 +642,36 @@ def test_transform_chunked_pipeline_equals_single_launch():
                 est.transform(bad)
     # the pipeline is intact after the failures
     assert_bitwise(est.transform(X).cpu().numpy(), ref, "transform after failures")
+
+
+@pytest.mark.parametrize("policy", ["fixed", "per-molecule-bbox"])
+def test_generate_batch_pipelined_equals_single_launch(policy, monkeypatch):
+    """generate_batch over a large batch (> PIPELINE_MIN_BATCH) runs through
+    the chunked pipeline (loader.generate_sets); grids, per-molecule GenStats
+    and per-index errors equal the single-launch path, with failed and empty
+    molecules spread over several chunks."""
+    from paper_2211_08506_b200 import gridgen
+
+    cfg = synth.CONFIGS[0]
+    spec = spec_of(cfg)
+    pb = synth.packed_batch(cfg, range(300))
+    sets = [vg.ParticleSet(pb.channels[a:b], pb.xyz.reshape(-1, 3)[a:b])
+            for a, b in zip(pb.offsets[:-1], pb.offsets[1:])]
+    sets[3] = vg.ParticleSet(np.zeros(0, np.int64), np.zeros((0, 3)))
+    sets[150] = vg.ParticleSet(np.array([0, 9]), np.ones((2, 3)))      # channel out of range
+    sets[299] = vg.ParticleSet(np.array([7]), np.ones((1, 3)))
+    got = vg.generate_batch(sets, spec, spec_policy=policy)
+    monkeypatch.setattr(gridgen, "PIPELINE_MIN_BATCH", 1 << 30)
+    ref = vg.generate_batch(sets, spec, spec_policy=policy)
+    assert sorted(got.errors) == sorted(ref.errors)
+    assert {150, 299} <= set(got.errors)
+    assert_bitwise(got.tensor.cpu().numpy(), ref.tensor.cpu().numpy(), f"pipelined {policy}")
+    for a, b in zip(got.results, ref.results):
+        assert (a is None) == (b is None)
+        if a is not None:
+            assert a[1].voxel_writes == b[1].voxel_writes
+            assert a[1].nonzero_voxels == b[1].nonzero_voxels
+            assert a[0].spec == b[0].spec
 
 
 def test_pipeline_edge_batches():

@@ -116,3 +116,48 @@ def test_bench_rejects_world_size_mismatch():
     res = _bench("--gpus", "3", "--dry-run", env={"WORLD_SIZE": "2", "RANK": "0"})
     assert res.returncode == 2
     assert "WORLD_SIZE=2" in res.stderr
+
+
+def _rank_shard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as tdist
+
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS[4]
+    counts = synth.atom_counts(cfg, range(300))
+    plain = shard.rank_shard(300)
+    balanced = shard.rank_shard(300, atom_counts=counts, grid_bytes=cfg.grid_bytes)
+    # every rank got a disjoint range; all-gathered they cover the batch
+    got = [None] * world
+    tdist.all_gather_object(got, (plain.start, plain.stop, balanced.start, balanced.stop))
+    tdist.destroy_process_group()
+    q.put((rank, shard.rank_world(), got))
+
+
+def test_rank_shard_under_a_process_group():
+    """shard.rank_shard reads rank / world from torch.distributed (the user's
+    DDP job): disjoint contiguous ranges covering the
+    batch, by count and by estimated cost."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = res[0][2]
+    assert got == res[1][2]
+    (a0, b0, c0, d0), (a1, b1, c1, d1) = got
+    assert (a0, b0, a1, b1) == (0, 150, 150, 300)
+    assert c0 == 0 and d0 == c1 and d1 == 300
+    assert res[0][1] == (0, 1)        # after destroy_process_group: the environment default
+
+
+def test_rank_world_from_environment(monkeypatch):
+    monkeypatch.setenv("RANK", "3")
+    monkeypatch.setenv("WORLD_SIZE", "8")
+    assert shard.rank_world() == (3, 8)
+    assert shard.rank_shard(80) == range(30, 40)
