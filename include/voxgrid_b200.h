@@ -25,7 +25,7 @@ extern "C" {
 #define VG_ERR_CUDA -2      /* a CUDA launch or runtime call failed             */
 #define VG_ERR_WORKSPACE -3 /* workspace pointer NULL or too small              */
 
-#define VG_ABI_VERSION 4
+#define VG_ABI_VERSION 5
 
 /* One batch of molecules in CSR form plus the grid geometry.
  *
@@ -90,6 +90,14 @@ int vg_workspace_layout(const vg_batch_desc* desc, vg_ws_layout* layout);
  * splat_atom (gridgen.py:97-109). stats (device [B]) may be NULL. */
 int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspace,
                     size_t workspace_bytes, vg_mol_stats* stats, void* stream);
+
+/* Which kernels vg_generate_f32 / vg_submit_f32 run for this batch into
+ * `out`: 1 = the one-launch small-batch kernel (K13: per-CTA axis tables in
+ * shared memory + gather; small molecules, output <= 4 MiB, open axes,
+ * D % 4 == 0, 16-byte aligned out), 0 = the tables kernel then the slab
+ * kernel (K1, K2 for large molecules, K3). Negative VG_ERR_* for an invalid
+ * descriptor. No GPU work. */
+int vg_fused_small(const vg_batch_desc* desc, const float* out);
 
 /* The second half of vg_generate_f32 alone: writes out[B, C, H, W, D] from
  * tables already computed into `workspace` by vg_axis_tables_f32 for the same

@@ -121,6 +121,7 @@ SIGNATURES = {
                                      ctypes.c_void_p]),
     "vg_axis_tables_f32": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]),
+    "vg_fused_small": (ctypes.c_int, [ctypes.POINTER(VgBatchDesc), ctypes.c_void_p]),
     "vg_erf_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_void_p]),
     "vg_fill_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_float,
@@ -160,7 +161,7 @@ SIGNATURES = {
     "vg_abi_version": (ctypes.c_int, []),
 }
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 _lib = None
 
 

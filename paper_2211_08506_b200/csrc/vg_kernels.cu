@@ -59,6 +59,10 @@ extern "C" int vg_internal_set_error(int code, const char* msg) {
   return set_error(code, "%s", msg);
 }
 
+// K13, the one-launch path of small batches (vg_small.cu)
+int vg_small_try(const vg_batch_desc* d, float* out, vg_mol_stats* stats, cudaStream_t st,
+                 bool stats_zeroed, bool dry_run);
+
 namespace {
 
 int check_launch(const char* what) {
@@ -324,6 +328,9 @@ __device__ __forceinline__ bool above_sat(float t) { return t >= VG_TSAT; }
 // lane), so each edge is evaluated once per pass.
 template <int T>
 __global__ void __launch_bounds__(kTableThreads) vg_tables_open_kernel(TableParams p) {
+  // a programmatic dependent (K3 in vg_generate_f32) may be scheduled now; it
+  // still waits for this grid's completion before reading the tables
+  asm volatile("griddepcontrol.launch_dependents;");
   constexpr int kRowsPerWarp = 32 / T;
   __shared__ float wbuf[kTableThreads / 32][kRowsPerWarp][kWin + 1];
   const int lane = threadIdx.x & 31;
@@ -1279,6 +1286,9 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   float* stage = reinterpret_cast<float*>(dyn4) + p.c0_cap;  // staged tables, then sublists
   const int tid = threadIdx.x, warp = tid >> 5;
 
+  // Launched as a programmatic dependent of K1 (vg_generate_f32): wait until
+  // K1 has completed and its tables are visible (a no-op otherwise).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   RowTile T;
   // Linear CTA index. Channel-fused CTAs: the tiles of one molecule are
   // adjacent, so the CTAs staging the same atoms' tables run close together
@@ -2347,6 +2357,10 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   return true;
 }
 
+// Set by vg_generate_f32 around its K3 launch: K3 directly follows K1 on the
+// same stream and may be launched as a programmatic dependent of it.
+thread_local bool g_pdl_launch = false;
+
 template <int M, int SW, int YP>
 int launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabParams& p) {
   // The row kernel is register-limited to 4 CTAs/SM; ask for the largest
@@ -2363,6 +2377,26 @@ int launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabPar
   });
   if (e != cudaSuccess)
     return set_error(VG_ERR_CUDA, "vg_slab_kernel attributes: %s", cudaGetErrorString(e));
+  if (g_pdl_launch) {
+    // programmatic dependent launch: K3's CTAs are scheduled while K1 (the
+    // previous kernel on this stream) finishes; K3 waits on griddepcontrol
+    // before it reads any table (vg_generate_f32 only)
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3((unsigned)nt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, vg_slab_kernel<M, SW, YP>, p);
+    if (le != cudaSuccess)
+      return set_error(VG_ERR_CUDA, "vg_slab_kernel (PDL): %s", cudaGetErrorString(le));
+    return VG_OK;
+  }
   vg_slab_kernel<M, SW, YP><<<grid, nt, smem, st>>>(p);
   return VG_OK;
 }
@@ -2824,10 +2858,30 @@ VG_API int vg_generate_f32(const vg_batch_desc* desc, float* out, void* workspac
   int rc = prepare(desc, out, workspace, workspace_bytes, &L);
   if (rc != VG_OK || desc->n_molecules == 0) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // small batches: tables and gather in one launch (K13, vg_small.cu)
+  rc = vg_small_try(desc, out, stats, st, false, false);
+  if (rc < 0) return rc;
+  if (rc == 1) return VG_OK;
   char* ws = static_cast<char*>(workspace);
+  // counters zeroed before K1, so that K3 directly follows K1 on the stream
+  // and can be launched as its programmatic dependent
+  if (stats != nullptr) {
+    const cudaError_t e = cudaMemsetAsync(stats, 0, sizeof(vg_mol_stats) * desc->n_molecules, st);
+    if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "stats memset: %s", cudaGetErrorString(e));
+  }
   rc = launch_tables(desc, L, ws, st);
   if (rc != VG_OK) return rc;
-  return launch_slabs(*desc, L, ws, out, stats, st);
+  g_pdl_launch = desc->n_atoms > 0 && env_int("VG_PDL", 1, 0, 1) == 1;
+  rc = launch_slabs(*desc, L, ws, out, stats, st, nullptr, false, true);
+  g_pdl_launch = false;
+  return rc;
+}
+
+VG_API int vg_fused_small(const vg_batch_desc* desc, const float* out) {
+  g_last_error[0] = '\0';
+  const int rc = validate(desc);
+  if (rc != VG_OK) return rc;
+  return vg_small_try(desc, const_cast<float*>(out), nullptr, nullptr, true, true) == 1 ? 1 : 0;
 }
 
 VG_API int vg_slabs_f32(const vg_batch_desc* desc, float* out, void* workspace,
@@ -2901,7 +2955,9 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   char* ws = static_cast<char*>(workspace);
   int kernels = 0;
   bool bins_ready = false;
-  if (B > 0 && n > 0) {
+  // small batches run K13 (tables + gather in one kernel) on the compute stream
+  const bool small = B > 0 && vg_small_try(desc, out, stats, ks, true, true) == 1;
+  if (B > 0 && n > 0 && !small) {
     rc = launch_tables(desc, L, ws, ts);
     if (rc != VG_OK) return rc;
     kernels = 1;
@@ -2918,7 +2974,11 @@ VG_API int vg_submit_f32(const vg_batch_desc* desc, const vg_submit_args* a, flo
   ok(cudaEventRecord(ev_tabled, ts));
   ok(cudaStreamWaitEvent(ks, ev_tabled, 0));
   if (e != cudaSuccess) return set_error(VG_ERR_CUDA, "submit (tables stage): %s", cudaGetErrorString(e));
-  if (B > 0) {
+  if (small) {
+    rc = vg_small_try(desc, out, stats, ks, stats_zeroed, false);
+    if (rc < 0) return rc;
+    kernels += 1;
+  } else if (B > 0) {
     rc = launch_slabs(*desc, L, ws, out, stats, ks, &kernels, bins_ready, stats_zeroed);
     if (rc != VG_OK) return rc;
   }

@@ -110,7 +110,6 @@ class GridEngine:
         self.device = _require_cuda(device)
         self.lib = _native.lib()
         self._ws = None
-        self.launches = 0  # kernels launched by this engine (2 per non-empty batch)
 
     def _workspace(self, nbytes: int):
         torch = _torch()
@@ -147,7 +146,8 @@ class GridEngine:
         return d
 
     def run(self, desc: _native.VgBatchDesc, out, stats=None, stream=None) -> None:
-        """Launch the two kernels (tables, slabs) for a filled descriptor."""
+        """Launch the path for a filled descriptor: K13 alone for a small batch,
+        else K1 (tables), K2 (bins, large molecules) and K3 (slabs)."""
         torch = _torch()
         layout = _native.VgWsLayout()
         _native.check(self.lib.vg_workspace_layout(desc, layout), "vg_workspace_layout")
@@ -157,8 +157,6 @@ class GridEngine:
                                       stats.data_ptr() if stats is not None else None,
                                       st.cuda_stream)
         _native.check(rc, "vg_generate_f32")
-        if desc.n_molecules:
-            self.launches += 2 if desc.n_atoms else 1
 
 
 _ENGINES: dict = {}

@@ -674,6 +674,79 @@ def test_generate_batch_pipelined_equals_single_launch(policy, monkeypatch):
             assert a[0].spec == b[0].spec
 
 
+def _small_vs_two_kernel(monkeypatch, offsets, ch, xyz, spec, **kw):
+    """The same batch through K13 (VG_SMALL=1) and through K1 + K3
+    (VG_SMALL=0): grids bit-identical, counters identical."""
+    monkeypatch.setenv("VG_SMALL", "1")
+    g1, s1 = vg.generate_packed(offsets, ch, xyz, spec, check=False, **kw)
+    g1, s1 = g1.cpu().numpy(), s1.cpu().numpy()
+    monkeypatch.setenv("VG_SMALL", "0")
+    g0, s0 = vg.generate_packed(offsets, ch, xyz, spec, check=False, **kw)
+    assert_bitwise(g1, g0.cpu().numpy(), "K13 vs K1+K3")
+    assert np.array_equal(s1, s0.cpu().numpy())
+    return g1, s1
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 32), (20, 18, 24), (7, 9, 12), (64, 64, 64),
+                                   (33, 5, 8), (1, 1, 4)])
+def test_small_kernel_equals_two_kernel_path(monkeypatch, shape):
+    """K13 (one launch: tables in shared memory + gather) against the
+    two-kernel path on random batches: shapes, empty molecules, thresholds,
+    per-molecule boxes, and molecules with more atoms of one channel than a
+    K13 pass holds (several compaction passes)."""
+    rng = np.random.default_rng(sum(shape))
+    B = 23
+    counts = rng.integers(0, 30, B)
+    counts[3] = 0
+    counts[5] = 300                                    # > one pass (cap <= 64)
+    offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    n = int(offsets[-1])
+    ch = rng.integers(0, 4, n).astype(np.int32)
+    ch[offsets[5]:offsets[6]] = 1                      # all in one channel
+    xyz = rng.uniform(-1, 9, (n, 3))
+    spec = vg.GridSpec(shape, 4, vg.BoundingBox((0.0, 0.0, 0.0), (8.0, 8.0, 8.0)), 0.45)
+    _small_vs_two_kernel(monkeypatch, offsets, ch, xyz, spec)
+    _small_vs_two_kernel(monkeypatch, offsets, ch, xyz, spec, threshold=1e-3)
+    _small_vs_two_kernel(monkeypatch, offsets, ch, xyz, spec, mode="dense")
+    mo = rng.uniform(-2, 1, (B, 3))
+    md = rng.uniform(0.1, 0.4, (B, 3))
+    _small_vs_two_kernel(monkeypatch, offsets, ch, xyz, spec, mol_origin=mo, mol_delta=md)
+
+
+def test_small_kernel_flags_invalid_device_atoms(monkeypatch):
+    """Device inputs with a channel outside [0, C) or a NaN coordinate: K13
+    skips the atom and flags its molecule exactly as K1 + K3 do."""
+    cfg = synth.CONFIGS[0]
+    pb = synth.packed_batch(cfg, range(6))
+    ch = pb.channels.copy()
+    xyz = pb.xyz.reshape(-1, 3).copy()
+    ch[pb.offsets[1]] = 9
+    xyz[pb.offsets[3] + 1, 2] = np.nan
+    off_d, ch_d, xyz_d = (torch.from_numpy(a).cuda() for a in (pb.offsets, ch, xyz))
+    g, st = _small_vs_two_kernel(monkeypatch, off_d, ch_d, xyz_d, spec_of(cfg))
+    assert list(np.flatnonzero(st[:, 0] < 0)) == [1, 3]
+
+
+def test_small_batches_take_the_one_launch_path(monkeypatch):
+    """A handful of cfg0 molecules (a few MB of grids) launch one kernel
+    (K13) instead of K1 + K3, and the result equals the oracle bit for bit."""
+    cfg = synth.CONFIGS[0]
+    pb = synth.packed_batch(cfg, range(4))
+    eng = vg.GridEngine()
+    monkeypatch.delenv("VG_SMALL", raising=False)
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        g, st = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec_of(cfg), engine=eng)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert any("vg_small_kernel" in n for n in names)
+    assert not any("vg_tables" in n or "vg_slab" in n for n in names)
+    ref, rs = orc.batch(pb.offsets, pb.channels, pb.xyz, geom_of(cfg), workers=orc.host_cores())
+    assert_bitwise(g.cpu().numpy(), ref, "cfg0 K13")
+    assert [int(v) for v in st[:, 1].cpu()] == [r["nonzero_voxels"] for r in rs]
+
+
 def test_pipeline_edge_batches():
     """GridPipeline over an empty batch, a batch of empty molecules and a
     periodic spec, reusing slots: every result equals the serial path and the
@@ -688,13 +761,13 @@ def test_pipeline_edge_batches():
     assert tuple(r0.grids.shape) == (0, 5, 32, 32, 32) and pipe.launches == 0
     r1 = pipe.submit(np.zeros(4, np.int64), np.zeros(0, np.int32), np.zeros((0, 3)))
     r1.ready.synchronize()
-    assert not r1.grids.any() and pipe.launches == 1          # K3 only (no atoms: no K1)
+    assert not r1.grids.any() and pipe.launches == 1          # one kernel, no tables
     pb = synth.packed_batch(cfg, range(5))
     r2 = pipe.submit(pb.offsets, pb.channels, pb.xyz)
     r2.ready.synchronize()
     g_ref, _ = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
     assert_bitwise(r2.grids.cpu().numpy(), g_ref.cpu().numpy(), "pipeline after empty")
-    assert pipe.launches == 3
+    assert pipe.launches == 2                                 # small batch: K13 alone
     cell = vg.LatticeCell((10.0, 10.0, 10.0))
     pspec = vg.GridSpec((32, 32, 32), 5, vg.BoundingBox((0, 0, 0), (10, 10, 10)), 0.5, cell)
     ppipe = GridPipeline(pspec)
