@@ -646,13 +646,29 @@ def run_b200(args):
         for _ in range(2):
             est.transform(X)[:, 0, 0, 0, 0].cpu()
         torch.cuda.synchronize()
+        # (a) blocking: every call's read-back waits for its grids
         t0 = time.perf_counter()
         for _ in range(K):
             est.transform(X)[:, 0, 0, 0, 0].cpu()
+        dt_sync = (time.perf_counter() - t0) / K
+        # (b) a loader's use: every call's read-back is queued (pinned host
+        # buffer, non-blocking) and the host validates and packs the next
+        # call while the device works; all read-backs complete before the clock
+        # stops
+        heads = torch.empty((K, Bl), dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(K):
+            heads[k].copy_(est.transform(X)[:, 0, 0, 0, 0], non_blocking=True)
+        torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / K
         transform = {"value": Bl / dt, "unit": "grids/s", "ms_per_step_wall": dt * 1e3,
+                     "value_blocking": Bl / dt_sync, "ms_per_step_wall_blocking": dt_sync * 1e3,
+                     "h2d_bytes_per_step": int(len(pb.channels) * 32),
+                     "d2h_bytes_per_step": Bl * 4,
                      "api": "paper_2211_08506_b200.GaussianVoxelizer.transform(list of (m,4) "
-                            "numpy arrays) + D2H of one voxel per grid"}
+                            "numpy arrays) + D2H of one voxel per grid: queued into pinned "
+                            "memory per call (value) or blocking per call (value_blocking)"}
 
     # per rank: molecules, pipelined ms/step, K3 ms, K3 GB/s (max-over-ranks
     # timing is what `value` uses; this shows the balance)

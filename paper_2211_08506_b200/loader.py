@@ -396,17 +396,20 @@ def _rows_chunk(part, C: int):
 
 
 def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", threshold=None,
-                  first: int = 128, max_chunk: int = 1 << 30):
+                  first: int = 1024, max_chunk: int = 8192):
     """Grids of a batch of (m_i, 4) host arrays of (channel, x, y, z) rows into
     one CUDA float32 tensor (B, C, H, W, D) — the fast path of
     ``GaussianVoxelizer.transform`` (estimator.py:134-151) for a shared box.
 
     The batch is cut into chunks (``first`` molecules, then doubling up to
-    ``max_chunk``; by default a short first chunk and the rest): each chunk is
-    validated and packed by the native packer straight into pinned staging
-    and written by the device into its slice of the output, so the device
-    starts after a short first chunk and the later chunks' copies and tables
-    (K1) overlap the HBM-bound slab kernel (K3) of the earlier ones.
+    ``max_chunk``): each chunk is validated and packed by the native packer
+    straight into pinned staging and written by the device into its slice of
+    the output, so on a large batch the device starts after the first chunk
+    and the later chunks' packing, copies and tables (K1) overlap the
+    HBM-bound slab kernel (K3) of the earlier ones. A batch of up to ``first``
+    molecules is one submission (every extra K3 launch costs a tail of idle
+    SMs; consecutive calls overlap anyway when the caller does not block on
+    each result).
     The caller's current stream is ordered after the last chunk on return.
     Returns None (after ordering any queued chunk) when a sample needs the
     per-sample path, which then raises the reference's error."""
@@ -424,10 +427,12 @@ def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", thres
     cur = torch.cuda.current_stream(dev)
     last = None
     with lock:
-        # `out` was allocated on the caller's stream: the copy stage (hence
-        # K1 and K3, which follow it) is ordered after the caller's work
+        # `out` was allocated on the caller's stream: the stage that writes it
+        # (K3, compute stream) is ordered after the caller's work; copies and
+        # tables do not touch it and may run ahead (beside the previous
+        # call's K3 and its read-back)
         pipe.start_event.record(cur)
-        pipe.copy_stream.wait_event(pipe.start_event)
+        pipe.compute_stream.wait_event(pipe.start_event)
         try:
             b, size = 0, max(1, first)
             while b < B:
@@ -467,7 +472,7 @@ def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", thres
 
 
 def generate_sets(sets, spec: GridSpec, counts, *, mol_origin=None, mol_delta=None, device=None,
-                  mode: str = "sparse", threshold=None, first: int = 64, max_chunk: int = 256):
+                  mode: str = "sparse", threshold=None, first: int = 1024, max_chunk: int = 8192):
     """``generate_batch``'s device work (gridgen.py:173-221) through the shared
     pipeline: ``(grids (B, C, H, W, D), stats (B, 2))`` CUDA tensors for
     validated ParticleSets, molecule b contributing ``counts[b]`` atoms (0 for
@@ -496,8 +501,11 @@ def generate_sets(sets, spec: GridSpec, counts, *, mol_origin=None, mol_delta=No
     cur = torch.cuda.current_stream(dev)
     last = None
     with lock:
-        pipe.start_event.record(cur)   # outputs and boxes were made on the caller's stream
-        pipe.copy_stream.wait_event(pipe.start_event)
+        # outputs (written by K3) and boxes (read by K1) were made on the
+        # caller's stream; the copies may run ahead
+        pipe.start_event.record(cur)
+        pipe.tables_stream.wait_event(pipe.start_event)
+        pipe.compute_stream.wait_event(pipe.start_event)
         try:
             b, size = 0, max(1, first)
             while b < B:

@@ -660,7 +660,16 @@ def test_generate_batch_pipelined_equals_single_launch(policy, monkeypatch):
     sets[3] = vg.ParticleSet(np.zeros(0, np.int64), np.zeros((0, 3)))
     sets[150] = vg.ParticleSet(np.array([0, 9]), np.ones((2, 3)))      # channel out of range
     sets[299] = vg.ParticleSet(np.array([7]), np.ones((1, 3)))
-    got = vg.generate_batch(sets, spec, spec_policy=policy)
+    import functools
+
+    from paper_2211_08506_b200 import loader
+
+    got = vg.generate_batch(sets, spec, spec_policy=policy)          # one submission
+    with monkeypatch.context() as m:                                 # many chunks
+        m.setattr(loader, "generate_sets",
+                  functools.partial(loader.generate_sets, first=7, max_chunk=50))
+        chunked = vg.generate_batch(sets, spec, spec_policy=policy)
+    assert_bitwise(chunked.tensor.cpu().numpy(), got.tensor.cpu().numpy(), "chunked sets")
     monkeypatch.setattr(gridgen, "PIPELINE_MIN_BATCH", 1 << 30)
     ref = vg.generate_batch(sets, spec, spec_policy=policy)
     assert sorted(got.errors) == sorted(ref.errors)
