@@ -179,3 +179,39 @@ def ctypes_sizeof_state():
     import ctypes
 
     return ctypes.sizeof(_native.VgDescentState)
+
+
+def _sass_by_function():
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([tool, "-sass", str(_native.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        if "Function : " in line:
+            cur = line.split("Function : ", 1)[1].strip()
+            funcs[cur] = []
+        elif cur is not None:
+            funcs[cur].append(line)
+    return funcs
+
+
+def test_accumulation_is_never_contracted_to_fma(lib):
+    """Bit parity needs acc + fl(fl(gy*gx)*gz) with two roundings: no kernel
+    that accumulates voxels may contain FFMA / FFMA2. (ptxas 12.9 contracts
+    mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite the rounding modifiers and
+    --fmad=false; the packed forms are not used, profiles/r2_fmul2_ab.txt.)
+    K1 / erf keep the FMAs of numpy's exp algorithm on purpose (vg_math.cuh)."""
+    funcs = _sass_by_function()
+    acc = {n: body for n, body in funcs.items()
+           if any(k in n for k in ("vg_slab_kernel", "vg_slab_generic_kernel",
+                                   "vg_slab_ws_kernel"))}
+    assert len(acc) >= 20, sorted(funcs)[:5]
+    for name, body in acc.items():
+        text = "\n".join(body)
+        assert "FFMA" not in text, name
+    for name, body in funcs.items():
+        if "vg_small_kernel" in name:
+            assert "FFMA2" not in "\n".join(body), name
