@@ -506,8 +506,6 @@ struct SlabParams {
   int fuse_channels;    // 1: one CTA serves every channel
   int cta_order;        // per-channel CTAs: 0 molecule fastest, 1 channel fastest
   int tasks;            // tiles per (molecule, channel): y-chunks x row-blocks x z-blocks
-  int tperm;            // > 0: tile order t -> t * tperm mod tasks (coprime), mixing
-                        // dense central tiles with sparse outer ones along the launch
   int n_molecules;
   int gx_win;           // staged gx rows per candidate (window), 0: all CTA rows
   int gx_wmax;          // rows one warp spans in a row step (window padding)
@@ -1322,7 +1320,6 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
       t = (int)tt;
     }
   }
-  if (p.tperm > 0) t = (int)(((unsigned long long)t * (unsigned)p.tperm) % (unsigned)p.tasks);
   if (p.z_blocks > 1) {
     zblk = t % p.z_blocks;
     t /= p.z_blocks;
@@ -2821,18 +2818,6 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.fuse_channels = fuse ? 1 : 0;
   p.cta_order = env_int("VG_ORDER", 0, 0, 1);
   p.tasks = p.n_jchunks * row_blocks * z_blocks;
-  // tile-order permutation (hook VG_TPERM = multiplier per mille of the tile
-  // count, made coprime; 0 = launch order)
-  {
-    const int pm = env_int("VG_TPERM", 0, 0, 999);
-    p.tperm = 0;
-    if (pm > 0 && p.tasks > 2) {
-      int m = (int)((int64_t)p.tasks * pm / 1000);
-      if (m < 2) m = 2;
-      while (gcd_int(m, p.tasks) != 1) ++m;
-      p.tperm = m % p.tasks;
-    }
-  }
   p.n_molecules = (int)d.n_molecules;
   const int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
   if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
