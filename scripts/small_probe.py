@@ -1,4 +1,4 @@
-"""cfg0 step time (vg_generate_f32, L2 flushed before each step, CUDA events
+"""Step time (default cfg0; args: config batch [variant ...], a variant = "VG_A=1 VG_B=2") (vg_generate_f32, L2 flushed before each step, CUDA events
 on the launch stream) for the K13 one-launch path and the K1 + K3 path, per
 VG_SMALL_K (float4 slots per thread)."""
 import json
@@ -32,8 +32,8 @@ ws = torch.empty(lay.total, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream().cuda_stream
 scratch = torch.empty(128 << 20, dtype=torch.float32, device=dev)
 alg = out.numel() * 4
-for variant in ("VG_SMALL=0 VG_PDL=0", "VG_SMALL=0", "VG_SMALL=0 VG_PDL=0 VG_K1T=4", "VG_SMALL=0 VG_K1T=4",
-                "VG_SMALL=1"):
+variants = sys.argv[3:] or ["VG_SMALL=0 VG_PDL=0", "VG_SMALL=0", "VG_SMALL=1"]
+for variant in variants:
     for kv in variant.split():
         k, v = kv.split("=")
         os.environ[k] = v
