@@ -86,3 +86,23 @@ def test_sets_pack_equals_numpy_packing(pk):
     assert rc in (0, -1)
     if rc == 0:
         assert np.array_equal(ch, odd.channels.astype(np.int32))
+
+
+def test_numpy_fallback_packer_matches_native(pk):
+    """loader._rows_chunk (the general path for inputs the native packer does
+    not take: lists, other dtypes) packs the same rows and rejects the same
+    values."""
+    from paper_2211_08506_b200.loader import _rows_chunk
+
+    pb = synth.packed_batch(synth.CONFIGS[0], range(20))
+    X = _rows(pb)
+    X32 = [x.astype(np.float32) for x in X]                  # float32 arrays
+    assert pk.rows_count(X32, 0, len(X32)) == -1             # not the native packer's
+    counts, rows = _rows_chunk(X32, 5)
+    assert np.array_equal(counts, np.diff(pb.offsets))
+    assert np.array_equal(rows, np.concatenate(X32).astype(np.float64))
+    got = _rows_chunk([x.tolist() for x in X[:3]], 5)      # nested lists
+    assert got is not None and np.array_equal(got[1], np.concatenate(X[:3]))
+    for bad in ([[5.0, 1, 1, 1]], [[0.5, 1, 1, 1]], [[-1.0, 1, 1, 1]], [[1.0, np.inf, 0, 0]],
+                [[1.0, 2.0, 3.0]]):
+        assert _rows_chunk([X[0], np.array(bad)], 5) is None
