@@ -153,6 +153,8 @@ class GridEngine:
         _native.check(self.lib.vg_workspace_layout(desc, layout), "vg_workspace_layout")
         ws = self._workspace(layout.total)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if stream is not None:
+            ws.record_stream(stream)   # a later, larger workspace frees it after this launch
         rc = self.lib.vg_generate_f32(desc, out.data_ptr(), ws.data_ptr(), ws.numel(),
                                       stats.data_ptr() if stats is not None else None,
                                       st.cuda_stream)

@@ -108,11 +108,22 @@ class GridPipeline:
         self.start_event = torch.cuda.Event()   # generate_rows / generate_sets ordering
 
     # -- buffers ---------------------------------------------------------------
+    def _own(self, t):
+        """Register a pipeline-owned device buffer with the pipeline's streams:
+        when it is dropped (reallocated larger, or a new batch size), the
+        caching allocator reuses its memory only after the work queued on
+        those streams up to then (e.g. the K3 of the slot's previous batch)
+        has finished, not merely in the allocating stream's order."""
+        for st in (self.copy_stream, self.tables_stream, self.compute_stream,
+                   self.readback_stream):
+            t.record_stream(st)
+        return t
+
     def _ensure(self, t, n, dtype, shape=None):
         torch = self.torch
         need = n if shape is None else int(np.prod(shape))
         if t is None or t.numel() < need or t.dtype != dtype:
-            t = torch.empty(max(need, 1), dtype=dtype, device=self.device)
+            t = self._own(torch.empty(max(need, 1), dtype=dtype, device=self.device))
         return t
 
     def _dev(self, t, dtype):
@@ -225,8 +236,8 @@ class GridPipeline:
                     check_packed(offsets, channels, xyz, spec.channels)
                 span = c0 + 4 * n
                 if slot.blk is None or slot.blk.numel() < span:
-                    slot.blk = torch.empty(max(span, 2 * staged[0].numel()), dtype=torch.uint8,
-                                           device=self.device)
+                    slot.blk = self._own(torch.empty(max(span, 2 * staged[0].numel()),
+                                                     dtype=torch.uint8, device=self.device))
                 dbase = slot.blk.data_ptr()
                 d_ptrs = (dbase, dbase + c0, dbase + x0)
             else:
@@ -263,7 +274,7 @@ class GridPipeline:
         desc.mol_origin = mol_origin.data_ptr() if mol_origin is not None else None
         desc.mol_delta = mol_delta.data_ptr() if mol_delta is not None else None
         if slot.out_b != B:
-            slot.stats = torch.empty((B, 2), dtype=torch.int64, device=self.device)
+            slot.stats = self._own(torch.empty((B, 2), dtype=torch.int64, device=self.device))
             slot.out = None
             slot.out_b = B
             slot.ptrs = None
@@ -275,13 +286,13 @@ class GridPipeline:
             grids = out
         else:
             if slot.out is None:
-                slot.out = torch.empty((B, spec.channels, H, W, D), dtype=torch.float32,
-                                       device=self.device)
+                slot.out = self._own(torch.empty((B, spec.channels, H, W, D),
+                                                 dtype=torch.float32, device=self.device))
                 slot.ptrs = None
             grids = slot.out
         args.h_stats = stats_out.data_ptr() if stats_out is not None else None
         if slot.ws is None:
-            slot.ws = torch.empty(1 << 20, dtype=torch.uint8, device=self.device)
+            slot.ws = self._own(torch.empty(1 << 20, dtype=torch.uint8, device=self.device))
             slot.ptrs = None
         if stats is not None:
             if (tuple(stats.shape) != (B, 2) or stats.dtype != torch.int64
@@ -297,7 +308,8 @@ class GridPipeline:
                          counters.data_ptr())
         rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)
         if rc == _native.VG_ERR_WORKSPACE and slot.ws_needed.value > slot.ws.numel():
-            slot.ws = torch.empty(slot.ws_needed.value, dtype=torch.uint8, device=self.device)
+            slot.ws = self._own(torch.empty(slot.ws_needed.value, dtype=torch.uint8,
+                                            device=self.device))
             slot.ptrs = (grids.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
                          counters.data_ptr())
             rc = self.lib.vg_submit_f32(desc, args, *slot.ptrs)

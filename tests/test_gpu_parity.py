@@ -756,6 +756,36 @@ def test_small_batches_take_the_one_launch_path(monkeypatch):
     assert [int(v) for v in st[:, 1].cpu()] == [r["nonzero_voxels"] for r in rs]
 
 
+def test_pipeline_varying_batch_sizes_without_syncs():
+    """Consecutive submissions of different sizes (every slot reallocates its
+    output, counters, inputs and workspace) queued with no host sync: each
+    result equals the serial path. Pipeline-owned buffers are registered with
+    the pipeline's streams, so a dropped buffer is not reused while an earlier
+    batch's kernels may still touch it."""
+    from paper_2211_08506_b200.loader import GridPipeline
+
+    cfg = synth.CONFIGS[0]
+    spec = spec_of(cfg)
+    pipe = GridPipeline(spec, depth=2)
+    sizes = [3, 40, 7, 64, 1, 33, 64, 2, 50, 9]
+    batches, results = [], []
+    start = 0
+    for n in sizes:
+        pb = synth.packed_batch(cfg, range(start, start + n))
+        start += n
+        batches.append(pb)
+        r = pipe.submit(pb.offsets, pb.channels, pb.xyz)
+        # keep a device copy of each result, ordered after its batch
+        pipe.compute_stream.wait_event(r.ready)
+        with torch.cuda.stream(pipe.compute_stream):
+            results.append((r.grids.clone(), r.stats.clone()))
+    torch.cuda.synchronize()
+    for pb, (g, st) in zip(batches, results):
+        g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+        assert_bitwise(g.cpu().numpy(), g_ref.cpu().numpy(), "varying sizes")
+        assert np.array_equal(st.cpu().numpy(), s_ref.cpu().numpy())
+
+
 def test_pipeline_edge_batches():
     """GridPipeline over an empty batch, a batch of empty molecules and a
     periodic spec, reusing slots: every result equals the serial path and the
