@@ -80,17 +80,20 @@ constexpr int kListCap = VG_LIST_CAP;  // K3: candidate segment capacity (staged
 constexpr int kC0CapMax = 1536;      // K3 row kernel: level-0 candidates kept per CTA (max)
 constexpr int kMaxCtaRows = 64;      // K3 row kernel: x rows per CTA (keeps staged rows short)
 constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
-constexpr int kRowThreads = 256;    // K3 row kernel: threads per CTA (upper bound)
+constexpr int kRowThreads = 512;     // K3 row kernel: threads per CTA (upper bound)
+constexpr int kWsThreads = 256;      // K3W: consumer threads per CTA
 #ifndef VG_ROW_MINB
-#define VG_ROW_MINB 4   // K3 row kernel: resident CTAs per SM the register budget targets
-#endif
+#define VG_ROW_MINB 4   // K3 row kernel: resident 256-thread CTAs per SM the register budget
+#endif                  // targets (64 registers; CTAs of up to 512 threads, 2 per SM)
 #ifndef VG_ROW_MINB1
 #define VG_ROW_MINB1 VG_ROW_MINB   // ... for one row step per CTA (M = 1)
 #endif
 #ifndef VG_WS_MINB
 #define VG_WS_MINB 3    // K3W: resident persistent CTAs per SM the register budget targets
 #endif
-constexpr int row_minb(int m) { return m == 1 ? VG_ROW_MINB1 : VG_ROW_MINB; }
+constexpr int row_minb(int m) {
+  return (m == 1 ? VG_ROW_MINB1 : VG_ROW_MINB) * 256 / kRowThreads;
+}
 constexpr int64_t kTaskBytes = 262144;       // K3: output bytes per CTA (y-chunk sizing)
 constexpr int64_t kFusedTaskBytes = 1048576; // ... per channel-fused CTA, all channels
 constexpr int64_t kMinCtas = 148 * 8;         // K3: CTAs a launch should at least offer
@@ -524,8 +527,11 @@ struct BinParams {
   int nb, nch, jc, C;
 };
 
+// The candidate list {x supp, y supp, z supp, atom} (kListCap + blockDim
+// entries: a compaction round may overshoot the cap by up to blockDim - 1)
+// lives in dynamic shared memory (row kernel) or a static array (generic
+// kernel) and is passed beside this struct.
 struct SlabShared {
-  int4 meta[kListCap + 256];          // {x supp, y supp, z supp, atom}; blockDim <= 256
   alignas(16) int warp_cnt[32];
   long long red[kMaxThreads / 32];
 };
@@ -571,12 +577,12 @@ struct AtomFilter {
   }
 };
 
-// Ordered compaction into sh.meta: scans source positions [pos, end) in
+// Ordered compaction into meta: scans source positions [pos, end) in
 // rounds of blockDim.x (position p is atom src[p], or atom p when src is
 // NULL) and appends, in ascending atom order, every atom passing `f`. Stops
 // once at least kListCap entries are held; `pos` returns the resume point.
-__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, const int* src,
-                          int64_t& pos, int64_t end, const AtomFilter& f) {
+__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int4* meta,
+                          const int* src, int64_t& pos, int64_t end, const AtomFilter& f) {
   int count = 0;
   while (pos < end && count < kListCap) {
     const int64_t p = pos + threadIdx.x;
@@ -590,7 +596,7 @@ __device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, const i
     }
     int total;
     const int rank = block_rank(keep, sh.warp_cnt, total);
-    if (keep) sh.meta[count + rank] = make_int4(s.x, s.y, s.z, (int)atom);
+    if (keep) meta[count + rank] = make_int4(s.x, s.y, s.z, (int)atom);
     count += total;
     pos += blockDim.x;
     __syncthreads();
@@ -598,10 +604,10 @@ __device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, const i
   return count;
 }
 
-__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int64_t& pos, int64_t a1,
-                          int c, int jlo, int jhi, int xa, int xb) {
+__device__ int build_list(const int4* __restrict__ supp, SlabShared& sh, int4* meta, int64_t& pos,
+                          int64_t a1, int c, int jlo, int jhi, int xa, int xb) {
   const AtomFilter f{c, jlo, jhi, xa, xb, 0, kMaxAxis};
-  return build_list(supp, sh, nullptr, pos, a1, f);
+  return build_list(supp, sh, meta, nullptr, pos, a1, f);
 }
 
 // Ordered compaction into c0 of the atoms listed in src[0, n) that pass f
@@ -748,6 +754,7 @@ template <bool VEC>
 __global__ void __launch_bounds__(256, 2) vg_slab_generic_kernel(const __grid_constant__ SlabParams p) {
   using Slot = typename SlotT<VEC>::T;
   __shared__ SlabShared sh;
+  __shared__ int4 gmeta[kListCap + 256];   // blockDim <= 256
   const int nt = blockDim.x;
 
   int64_t t = blockIdx.x;
@@ -764,7 +771,7 @@ __global__ void __launch_bounds__(256, 2) vg_slab_generic_kernel(const __grid_co
   const int slot0 = sb * nt * p.m_steps;
 
   int64_t pos = a0;
-  const int n_list = build_list(p.supp, sh, pos, a1, c, j0, j1, 0, kMaxAxis);
+  const int n_list = build_list(p.supp, sh, gmeta, pos, a1, c, j0, j1, 0, kMaxAxis);
   const bool single = pos >= a1;  // every candidate of the chunk fits the list
 
   float* out_c = p.out + ((b * p.C + c) * (int64_t)p.H) * p.slab_elems;
@@ -779,15 +786,15 @@ __global__ void __launch_bounds__(256, 2) vg_slab_generic_kernel(const __grid_co
       Slot acc;
       zero_slot(acc);
       if (single) {
-        gather_slot<VEC>(p, sh.meta, n_list, j, valid, i, k, acc);
+        gather_slot<VEC>(p, gmeta, n_list, j, valid, i, k, acc);
       } else {
         // Overflow path (chunks with > kListCap candidates): rebuild the
         // slab's list segment by segment; order across segments is ascending.
         int64_t pos2 = a0;
         while (pos2 < a1) {
           __syncthreads();
-          const int n2 = build_list(p.supp, sh, pos2, a1, c, j, j + 1, 0, kMaxAxis);
-          gather_slot<VEC>(p, sh.meta, n2, j, valid, i, k, acc);
+          const int n2 = build_list(p.supp, sh, gmeta, pos2, a1, c, j, j + 1, 0, kMaxAxis);
+          gather_slot<VEC>(p, gmeta, n2, j, valid, i, k, acc);
         }
         __syncthreads();
       }
@@ -1282,8 +1289,9 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   constexpr int kWidth = SW;
   __shared__ SlabShared sh;
   extern __shared__ float4 dyn4[];
-  int* c0 = reinterpret_cast<int*>(dyn4);             // level-0 candidates [c0_cap]
-  float* stage = reinterpret_cast<float*>(dyn4) + p.c0_cap;  // staged tables, then sublists
+  int4* meta_l = reinterpret_cast<int4*>(dyn4);       // candidate list [kListCap + blockDim]
+  int* c0 = reinterpret_cast<int*>(meta_l + kListCap + blockDim.x);  // level-0 [c0_cap]
+  float* stage = reinterpret_cast<float*>(c0) + p.c0_cap;  // staged tables, then sublists
   const int tid = threadIdx.x, warp = tid >> 5;
 
   // Launched as a programmatic dependent of K1 (vg_generate_f32): wait until
@@ -1370,15 +1378,15 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
     c_hi = p.C;
     const AtomFilter fa{-1, j0, j1, T.row_base, T.row_end, T.zv0, T.zv1};
     int64_t pos = T.a0;
-    const int n = build_list(p.supp, sh, nullptr, pos, T.a1, fa);
+    const int n = build_list(p.supp, sh, meta_l, nullptr, pos, T.a1, fa);
     if (pos >= T.a1 && n <= p.stage_cap) {
-      stage_tables<SW>(p, sh.meta, n, stage, j0, j1, T.row_base, rows, T.zv0, T.zv1);
+      stage_tables<SW>(p, meta_l, n, stage, j0, j1, T.row_base, rows, T.zv0, T.zv1);
       cp_async_wait_all();
       __syncthreads();
       float* out_b = p.out + T.b * p.C * chan_elems + j0 * p.slab_elems + slot0;
       for (int c = 0; c < p.C; ++c) {
         Counts<M> cnt;
-        build_sublists<M>(p, sh.meta, n, c, lists, stage_s, j0, j1, T.row_base, rlo0, rhi0, R, cnt);
+        build_sublists<M>(p, meta_l, n, c, lists, stage_s, j0, j1, T.row_base, rlo0, rhi0, R, cnt);
         __syncwarp();
         nz += accumulate<M, SW, YP, true>(out_b + c * chan_elems, p.slab_elems, R * p.D, j1 - j0,
                                            ibase, T.row_end, R, cnt, lists_s, p.stage_cap, gx_off,
@@ -1422,7 +1430,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
       const int je = min(j1, js + sc);
       const AtomFilter f{c, js, je, T.row_base, T.row_end, T.zv0, T.zv1};
       int64_t pos = src_begin;
-      int n = build_list(p.supp, sh, src, pos, src_end, f);
+      int n = build_list(p.supp, sh, meta_l, src, pos, src_end, f);
       if (rounds == 0) VG_TS(8);
       if ((pos < src_end || n > p.stage_cap) && sc > 1) {  // uniform: halve the sub-chunk, rebuild
         sc = (sc + 1) >> 1;
@@ -1436,7 +1444,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
         // n == 0 still runs one pass: every slot is stored (as zero) exactly once
         for (int s0 = 0; s0 < max(n, 1); s0 += p.stage_cap) {
           const int ns = min(p.stage_cap, n - s0);
-          const int4* meta = sh.meta + s0;
+          const int4* meta = meta_l + s0;
           stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
           Counts<M> cnt;
           build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, T.row_base, rlo0, rhi0, R, cnt);
@@ -1464,7 +1472,7 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
           first = false;
         }
         if (pos >= src_end) break;
-        n = build_list(p.supp, sh, src, pos, src_end, f);
+        n = build_list(p.supp, sh, meta_l, src, pos, src_end, f);
       }
       js = je;
     }
@@ -1675,7 +1683,7 @@ struct WsProdShared {
 constexpr int kWsMaxUnits = 17;   // slab pairs per tile (jc <= 32) + 1
 
 template <int M, int NP>
-__global__ void __launch_bounds__(kRowThreads + 32 * NP, VG_WS_MINB)
+__global__ void __launch_bounds__(kWsThreads + 32 * NP, VG_WS_MINB)
     vg_slab_ws_kernel(const __grid_constant__ SlabParams p, int* tile_counter, int n_tiles,
                       int kWsStages) {
   constexpr int SW = 8, YP = 2;
@@ -2339,13 +2347,17 @@ bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   for (int q = 1; base * q <= kRowThreads; ++q) {
     if (fq != 0 && fq != q) continue;
     const int t = base * q, r = t / spr;
+    if (r > kMaxCtaRows && base * q > 256) continue;   // wider CTAs only up to 64 rows
     const int need = (W + r - 1) / r;
     int m = need < 8 ? need : 8;
     const int mcap = kMaxCtaRows / r > 1 ? kMaxCtaRows / r : 1;
     if (m > mcap) m = mcap;
     const int rb = (need + m - 1) / m;
     const double waste = (double)(rb * m * r - W) / (rb * m * r);
-    const double score = waste + (t < 128 ? 0.25 : 0.0) + fabs(t - 256.0) * 1e-5;
+    // least padding; then fewer row steps per CTA (more threads: 512-thread
+    // CTAs of one step beat 256-thread CTAs of two at cfg1, 288 threads
+    // cover cfg4's 48 rows exactly; measured on B200), then nearest 256
+    const double score = waste + (t < 128 ? 0.25 : 0.0) + (m - 1) * 1e-3 + fabs(t - 256.0) * 1e-6;
     if (score < best) {
       best = score;
       *nt = t;
@@ -2372,7 +2384,7 @@ int launch_rows_m(dim3 grid, int nt, size_t smem, cudaStream_t st, const SlabPar
                                          cudaSharedmemCarveoutMaxShared);
     if (r == cudaSuccess)
       r = cudaFuncSetAttribute(vg_slab_kernel<M, SW, YP>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     return r;
   });
   if (e != cudaSuccess)
@@ -2531,7 +2543,7 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
 bool want_bins(const vg_batch_desc& d, const SlabPlan& P) {
   if (env_int("VG_BINS", 1, 0, 1) == 0) return false;
   if (!P.rows_ok || P.fuse || d.periodic) return false;
-  if (P.mean_atoms <= 2 * kRowThreads) return false;
+  if (P.mean_atoms <= 512) return false;
   const int64_t nb = (int64_t)d.C * P.n_jchunks;
   return nb <= kMaxBins && (int64_t)d.n_atoms * P.n_jchunks <= (int64_t)1 << 28;
 }
@@ -2759,7 +2771,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   // slab pairs, even y-chunks so every unit starts on an even slab, 16-byte
   // aligned x rows for the bulk copies). VG_WS=0 keeps vg_slab_kernel.
   if (p.bins != nullptr && !fuse && sw == 8 && yp == 2 && M <= 2 && jc % 2 == 0 &&
-      (M * R) % 4 == 0 && env_int("VG_WS", 0, 0, 1) == 1) {
+      (M * R) % 4 == 0 && nt <= kWsThreads && env_int("VG_WS", 0, 0, 1) == 1) {
     // VG_WS_M=2: two row steps per tile (twice the rows per producer pass)
     int Mw = M, rbw = row_blocks;
     if (M == 1 && env_int("VG_WS_M", 1, 1, 2) == 2 && 2 * R <= 255) {
@@ -2797,7 +2809,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int64_t per_cand = 4 * (int64_t)p.stage_stride + (int64_t)(nt / 32) * M * sizeof(int2);
   auto cap_at = [&](int blocks) {
     const int64_t budget = (int64_t)228 * 1024 / blocks - 1024 - (int64_t)sizeof(SlabShared) -
-                           (int64_t)p.c0_cap * 4 - (int64_t)(M * R + 8 + 3) * 4;
+                           (int64_t)(kListCap + nt) * 16 - (int64_t)p.c0_cap * 4 -
+                           (int64_t)(M * R + 8 + 3) * 4;
     return budget / per_cand;
   };
   // With 5 or more CTAs per SM, one CTA fewer is worth it when it lifts the
@@ -2813,7 +2826,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   // slack: rows >= W of the last step read (and discard) past the last block;
   // then the warp-private sublists (int2 per candidate, row step and warp)
   p.stage_floats = (p.stage_cap * p.stage_stride + M * R + 8 + 3) & ~3;
-  const size_t smem = (size_t)p.c0_cap * sizeof(int) + (size_t)p.stage_floats * sizeof(float) +
+  const size_t smem = (size_t)(kListCap + nt) * sizeof(int4) + (size_t)p.c0_cap * sizeof(int) +
+                      (size_t)p.stage_floats * sizeof(float) +
                       (size_t)(nt / 32) * M * p.stage_cap * sizeof(int2);
   p.fuse_channels = fuse ? 1 : 0;
   p.cta_order = env_int("VG_ORDER", 0, 0, 1);
