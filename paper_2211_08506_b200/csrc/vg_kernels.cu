@@ -2342,31 +2342,38 @@ int gcd_int(int a, int b) { return b == 0 ? a : gcd_int(b, a % b); }
 bool plan_rows(int spr, int W, int* nt, int* R, int* M, int* row_blocks) {
   const int base = spr / gcd_int(32, spr) * 32;  // lcm(32, spr)
   if (base > kRowThreads) return false;
-  double best = 1e30;
-  int fq = env_int("VG_PLAN_Q", 0, 1, kRowThreads / base);   // hook: force the thread multiple
-  for (int q = 1; base * q <= kRowThreads; ++q) {
-    if (fq != 0 && fq != q) continue;
-    const int t = base * q, r = t / spr;
-    if (r > kMaxCtaRows && base * q > 256) continue;   // wider CTAs only up to 64 rows
-    const int need = (W + r - 1) / r;
-    int m = need < 8 ? need : 8;
-    const int mcap = kMaxCtaRows / r > 1 ? kMaxCtaRows / r : 1;
-    if (m > mcap) m = mcap;
-    const int rb = (need + m - 1) / m;
-    const double waste = (double)(rb * m * r - W) / (rb * m * r);
-    // least padding; then fewer row steps per CTA (more threads: 512-thread
-    // CTAs of one step beat 256-thread CTAs of two at cfg1, 288 threads
-    // cover cfg4's 48 rows exactly; measured on B200), then nearest 256
-    const double score = waste + (t < 128 ? 0.25 : 0.0) + (m - 1) * 1e-3 + fabs(t - 256.0) * 1e-6;
-    if (score < best) {
-      best = score;
-      *nt = t;
-      *R = r;
-      *M = m;
-      *row_blocks = rb;
+  // CTAs of t = base * q threads, r = t / spr rows per step, m steps
+  auto scan = [&](int forced) {
+    double best = 1e30;
+    for (int q = 1; base * q <= kRowThreads; ++q) {
+      if (forced != 0 && forced != q) continue;
+      const int t = base * q, r = t / spr;
+      if (r > kMaxCtaRows && t > 256) continue;   // wider CTAs only up to 64 rows
+      const int need = (W + r - 1) / r;
+      int m = need < 8 ? need : 8;
+      const int mcap = kMaxCtaRows / r > 1 ? kMaxCtaRows / r : 1;
+      if (m > mcap) m = mcap;
+      const int rb = (need + m - 1) / m;
+      const double waste = (double)(rb * m * r - W) / (rb * m * r);
+      // least padding; then fewer row steps per CTA (512-thread CTAs of one
+      // step beat 256-thread CTAs of two at cfg1, 288 threads cover cfg4's
+      // 48 rows exactly; measured on B200), then the count nearest 256
+      const double score =
+          waste + (t < 128 ? 0.25 : 0.0) + (m - 1) * 1e-3 + fabs(t - 256.0) * 1e-6;
+      if (score < best) {
+        best = score;
+        *nt = t;
+        *R = r;
+        *M = m;
+        *row_blocks = rb;
+      }
     }
-  }
-  return true;
+    return best < 1e30;
+  };
+  // hook VG_PLAN_Q: force the thread multiple (a multiple the rules reject
+  // falls back to the free choice)
+  const int fq = env_int("VG_PLAN_Q", 0, 1, kRowThreads / base);
+  return (fq != 0 && scan(fq)) || scan(0);
 }
 
 // Set by vg_generate_f32 around its K3 launch: K3 directly follows K1 on the

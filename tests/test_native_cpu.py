@@ -109,6 +109,28 @@ def test_invalid_descriptor_reports_error_without_gpu(lib):
     assert layout.total >= 256 and layout.row_x == 8
 
 
+def test_launch_planning_every_forced_cta_width(lib, monkeypatch):
+    """The K3 launch plan (run by vg_workspace_layout on the host, no GPU)
+    for every forced thread multiple VG_PLAN_Q, including ones its rules
+    reject (they fall back to the free choice instead of leaving the plan
+    empty), and every shape class of the BASELINE configs."""
+    d = _native.VgBatchDesc()
+    d.C = 5
+    d.scale = 1.0
+    d.offsets = 8   # any non-NULL pointer; planning never dereferences it
+    layout = _native.VgWsLayout()
+    for shape in ((32, 32, 32), (64, 64, 64), (48, 48, 48), (128, 128, 128), (5, 7, 9)):
+        d.H, d.W, d.D = shape
+        d.delta[:] = (0.3, 0.3, 0.3)
+        for atoms in (19, 2000):
+            d.n_molecules, d.n_atoms = 4, 4 * atoms
+            d.xyz = d.channel = 8
+            for q in ("", "1", "2", "3", "4", "5", "8", "16"):
+                monkeypatch.setenv("VG_PLAN_Q", q)
+                assert lib.vg_workspace_layout(ctypes.byref(d), ctypes.byref(layout)) == 0
+                assert layout.total >= 256
+
+
 def test_erf_saturation_threshold(lib):
     """K1 skips the series where E(t) is exactly +-1: E(t) == 1.0f for every
     float32 t >= t_sat (checked on every float in [t_sat, t_sat*4) and a
