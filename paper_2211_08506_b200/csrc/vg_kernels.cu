@@ -2169,10 +2169,17 @@ __global__ void vg_erf_kernel(const float* __restrict__ t, float* __restrict__ o
 // Write-ceiling probe: grid-stride streaming 128-bit stores (as K3 stores).
 // (scripts/probes/write_ceiling.cu: this pattern with 148*64 CTAs is the
 // fastest of the simple write patterns on B200, ~6.87 TB/s.)
-__global__ void vg_fill_kernel(float4* __restrict__ out, int64_t n4, float4 v) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x)
-    __stcs(out + i, v);
+// One 16 KiB block of streaming float4 stores per CTA (4 per thread, each
+// warp instruction 512 contiguous bytes), as many CTAs as blocks: 7.5 TB/s on
+// B200, above a grid-stride sweep of the same stores (7.0) and torch's fill_
+// (7.4) (scripts/fill_probe.py, profiles/r2_write_ceiling.txt).
+__global__ void __launch_bounds__(256) vg_fill_kernel(float4* __restrict__ out, int64_t n4, float4 v) {
+  const int64_t base = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t i = base + k * 256;
+    if (i < n4) __stcs(out + i, v);
+  }
 }
 
 __global__ void vg_fill_tail_kernel(float* __restrict__ out, int64_t n, float v) {
@@ -3044,8 +3051,8 @@ VG_API int vg_fill_f32(float* out, int64_t n, float value, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n4 = n / 4;
   if (n4 > 0) {
-    int64_t blocks = (n4 + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
+    const int64_t blocks = (n4 + 1023) / 1024;
+    if (blocks > INT_MAX) return set_error(VG_ERR_INVALID, "fill too large");
     vg_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(out), n4,
                                                       make_float4(value, value, value, value));
   }
