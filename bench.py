@@ -575,7 +575,7 @@ def run_b200(args):
         pipe.begin(pa)
         for _ in range(K):
             pipe.submit(off_d, ch_d, xyz_d)
-        pb_.record(pipe.compute_stream)
+        pb_.record(pipe.join())   # after the K3s of every slot's compute stream
         torch.cuda.synchronize()
     pipe_ms = pa.elapsed_time(pb_)
     t_max = dist.max(pipe_ms)

@@ -6,7 +6,7 @@ separate CUDA streams:
 
     copy stream     H2D of batch k+1's atoms (pinned host -> device)
     tables stream   K1 (per-atom axis tables) and K2 (bins) of batch k+1
-    compute stream  K3 (slab gather/store) of batch k   <- HBM-bound
+    compute streams K3 (slab gather/store) of batch k   <- HBM-bound
 
 K1/K2 are compute-bound and K3 HBM-bound, so running them concurrently
 hides most of K1 and the copies behind the grid writes. One native call per
@@ -15,17 +15,25 @@ Inputs, table workspaces and outputs are buffered per slot (``depth``, 2 by
 default); a slot's copy stage waits for its previous K3, so results are
 identical to the serial path (bit for bit: same kernels, same inputs).
 
-The caller consumes ``result.grids`` on ``pipeline.compute_stream`` (or
-after ``result.ready.synchronize()``); a slot is rewritten ``depth``
-submissions later, after the caller's ``release`` event (optional) and the
-previous consumer-visible event.
+Every slot has its own compute stream: consecutive K3s write different
+buffers, so nothing orders them but their inputs, and the first CTAs of
+batch k+1's K3 are dispatched into the SM slots that batch k's last CTAs
+leave idle (a K3 alone ends with a tail of partly idle SMs: ~20 us per
+launch, 2-3% of a cfg1 step and 15% of a 128-molecule step). Submissions
+that write overlapping caller buffers (``out=``) stay ordered.
+
+The caller consumes ``result.grids`` after ``result.ready`` (wait for the
+event on the consuming stream, or ``result.ready.synchronize()``); a slot is
+rewritten ``depth`` submissions later, after the caller's ``release`` event
+(optional) and the previous consumer-visible event.
 """
 
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
-from collections import OrderedDict
+from collections import OrderedDict, deque
 from dataclasses import dataclass
 
 import numpy as np
@@ -41,7 +49,7 @@ __all__ = ["GridPipeline", "PipelineResult", "shared_pipeline", "generate_rows",
 class PipelineResult:
     grids: object        # torch.float32 CUDA (B, C, H, W, D); valid after `ready`
     stats: object        # torch.int64 CUDA (B, 2): voxel_writes, nonzero_voxels
-    ready: object        # torch.cuda.Event recorded on the compute stream
+    ready: object        # torch.cuda.Event recorded after the batch's K3 (and read-back)
     slot: int
 
     def check(self) -> None:
@@ -98,10 +106,16 @@ class GridPipeline:
             # instead of queueing behind K3's whole grid
             self.copy_stream = torch.cuda.Stream(self.device)
             self.tables_stream = torch.cuda.Stream(self.device, priority=-1)
-            self.compute_stream = torch.cuda.Stream(self.device)
+            # one compute stream per slot: the next batch's K3 fills the SM
+            # slots the previous K3's tail leaves idle (VG_PIPE_STREAMS=1: one
+            # stream, K3s strictly one after the other)
+            n_cs = max(1, min(depth, int(os.environ.get("VG_PIPE_STREAMS", depth) or depth)))
+            self.compute_streams = [torch.cuda.Stream(self.device) for _ in range(n_cs)]
+            self.compute_stream = self.compute_streams[0]   # primary (join() target)
             # stats read-back beside the next batch's K3 (keeps K3s back to back)
             self.readback_stream = torch.cuda.Stream(self.device)
         self.slots = [_Slot() for _ in range(depth)]
+        self._recent = deque(maxlen=depth)   # (out range, done event, stream) of the last submits
         self.k = 0
         self.launches = 0
         self.atoms_per_mol = 32.0      # staging estimate of generate_rows
@@ -114,7 +128,7 @@ class GridPipeline:
         caching allocator reuses its memory only after the work queued on
         those streams up to then (e.g. the K3 of the slot's previous batch)
         has finished, not merely in the allocating stream's order."""
-        for st in (self.copy_stream, self.tables_stream, self.compute_stream,
+        for st in (self.copy_stream, self.tables_stream, *self.compute_streams,
                    self.readback_stream):
             t.record_stream(st)
         return t
@@ -174,22 +188,24 @@ class GridPipeline:
         checked (``check_packed``) by the caller."""
         torch = self.torch
         spec = self.spec
-        slot = self.slots[self.k % len(self.slots)]
+        idx = self.k % len(self.slots)
+        slot = self.slots[idx]
         self.k += 1
+        cstream = self.compute_streams[idx % len(self.compute_streams)]
         B = int(offsets.shape[0]) - 1
         n = int(channels.shape[0])
         H, W, D = spec.shape
         if release is not None:
-            for st in (self.copy_stream, self.tables_stream, self.compute_stream):
+            for st in (self.copy_stream, self.tables_stream, *self.compute_streams):
                 st.wait_event(release)
         if slot.events is None:
             slot.events = [torch.cuda.Event() for _ in range(4)]   # copied, tabled, done, read
             for ev in slot.events:   # torch creates the cudaEvent_t on first record
-                ev.record(self.compute_stream)
+                ev.record(cstream)
             slot.args = _native.VgSubmitArgs()
             slot.args.copy_stream = self.copy_stream.cuda_stream
             slot.args.tables_stream = self.tables_stream.cuda_stream
-            slot.args.compute_stream = self.compute_stream.cuda_stream
+            slot.args.compute_stream = cstream.cuda_stream
             slot.args.ev_copied = slot.events[0].cuda_event
             slot.args.ev_tabled = slot.events[1].cuda_event
             slot.args.ev_done = slot.events[2].cuda_event
@@ -218,7 +234,7 @@ class GridPipeline:
             for t, src in ((off_d, offsets), (ch_d, channels), (xyz_d, xyz)):
                 if t is not src:   # our conversion: its memory must outlive the kernels
                     t.record_stream(self.tables_stream)
-                    t.record_stream(self.compute_stream)
+                    t.record_stream(cstream)
             args.h_offsets = args.h_channel = args.h_xyz = None
             host = (off_d, ch_d, xyz_d)
             d_ptrs = (off_d.data_ptr(), ch_d.data_ptr(), xyz_d.data_ptr())
@@ -302,6 +318,16 @@ class GridPipeline:
             counters = stats
         else:
             counters = slot.stats
+        if out is not None or stats is not None:
+            # caller buffers: a K3 that rewrites memory an earlier, still
+            # recent submission wrote on another compute stream follows it
+            lo, hi = grids.data_ptr(), grids.data_ptr() + grids.numel() * 4
+            slo, shi = counters.data_ptr(), counters.data_ptr() + counters.numel() * 8
+            for (a0, a1, b0, b1, ev, st) in self._recent:
+                if st is not cstream and ((lo < a1 and a0 < hi) or (slo < b1 and b0 < shi)):
+                    cstream.wait_event(ev)
+                if slo < b1 and b0 < shi:   # the counters are cleared on the tables stream
+                    self.tables_stream.wait_event(ev)
         if (slot.ptrs is None or slot.ptrs[0] != grids.data_ptr()
                 or slot.ptrs[3] != counters.data_ptr()):
             slot.ptrs = (grids.data_ptr(), slot.ws.data_ptr(), slot.ws.numel(),
@@ -317,6 +343,9 @@ class GridPipeline:
         self.launches += slot.kernels.value   # K1, K2 (binned batches), K3
         slot.read_back = stats_out is not None and B > 0
         ready = slot.events[3] if slot.read_back else slot.events[2]
+        self._recent.append((grids.data_ptr(), grids.data_ptr() + grids.numel() * 4,
+                             counters.data_ptr(), counters.data_ptr() + counters.numel() * 8,
+                             slot.events[2], cstream))
         # keep the inputs alive until the copy / kernels have read them
         slot._host = host
         slot._boxes = (mol_origin, mol_delta)
@@ -324,12 +353,26 @@ class GridPipeline:
 
     def begin(self, event):
         """Make every stage wait for ``event`` (e.g. the start of a timed region)."""
-        for st in (self.copy_stream, self.tables_stream, self.compute_stream,
+        for st in (self.copy_stream, self.tables_stream, *self.compute_streams,
                    self.readback_stream):
             st.wait_event(event)
 
+    def order_after(self, stream):
+        """Order every later K3 (any compute stream) after the work already
+        queued on ``stream`` (the producer of a caller-owned output)."""
+        for st in self.compute_streams:
+            st.wait_stream(stream)
+
+    def join(self):
+        """Order ``compute_stream`` (the primary one) after every K3 queued so
+        far, and return it: an event recorded on it then marks the end of all
+        submitted batches."""
+        for st in self.compute_streams[1:]:
+            self.compute_stream.wait_stream(st)
+        return self.compute_stream
+
     def synchronize(self):
-        for st in (self.copy_stream, self.tables_stream, self.compute_stream,
+        for st in (self.copy_stream, self.tables_stream, *self.compute_streams,
                    self.readback_stream):
             st.synchronize()
 
@@ -422,7 +465,7 @@ def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", thres
     molecules is one submission (every extra K3 launch costs a tail of idle
     SMs; consecutive calls overlap anyway when the caller does not block on
     each result).
-    The caller's current stream is ordered after the last chunk on return.
+    The caller's current stream is ordered after every chunk on return.
     Returns None (after ordering any queued chunk) when a sample needs the
     per-sample path, which then raises the reference's error."""
     torch = _torch()
@@ -438,13 +481,15 @@ def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", thres
         X = list(X)
     cur = torch.cuda.current_stream(dev)
     last = None
+    tail = deque(maxlen=len(pipe.compute_streams))
     with lock:
         # `out` was allocated on the caller's stream: the stage that writes it
         # (K3, compute stream) is ordered after the caller's work; copies and
         # tables do not touch it and may run ahead (beside the previous
         # call's K3 and its read-back)
         pipe.start_event.record(cur)
-        pipe.compute_stream.wait_event(pipe.start_event)
+        for st in pipe.compute_streams:
+            st.wait_event(pipe.start_event)
         try:
             b, size = 0, max(1, first)
             while b < B:
@@ -476,10 +521,12 @@ def generate_rows(X, spec: GridSpec, *, device=None, mode: str = "sparse", thres
                     ch[:] = rows[:, 0]
                     xyz[:] = rows[:, 1:4]
                 last = pipe.submit(off, ch, xyz, out=out[b:e], validated=True)
+                tail.append(last.ready)
                 b, size = e, min(2 * size, max(max_chunk, 1))
         finally:
-            if last is not None:
-                cur.wait_event(last.ready)
+            # every compute stream's last chunk (each stream runs in order)
+            for ev in tail:
+                cur.wait_event(ev)
     return out
 
 
@@ -512,12 +559,14 @@ def generate_sets(sets, spec: GridSpec, counts, *, mol_origin=None, mol_delta=No
         sets = list(sets)
     cur = torch.cuda.current_stream(dev)
     last = None
+    tail = deque(maxlen=len(pipe.compute_streams))
     with lock:
         # outputs (written by K3) and boxes (read by K1) were made on the
         # caller's stream; the copies may run ahead
         pipe.start_event.record(cur)
         pipe.tables_stream.wait_event(pipe.start_event)
-        pipe.compute_stream.wait_event(pipe.start_event)
+        for st in pipe.compute_streams:
+            st.wait_event(pipe.start_event)
         try:
             b, size = 0, max(1, first)
             while b < B:
@@ -540,10 +589,11 @@ def generate_sets(sets, spec: GridSpec, counts, *, mol_origin=None, mol_delta=No
                     mo, md = boxes[0][b:e], boxes[1][b:e]
                 last = pipe.submit(off, ch, xyz, out=out[b:e], stats=stats[b:e],
                                    mol_origin=mo, mol_delta=md, validated=True)
+                tail.append(last.ready)
                 b, size = e, min(2 * size, max(max_chunk, 1))
         finally:
-            if last is not None:
-                cur.wait_event(last.ready)
+            for ev in tail:
+                cur.wait_event(ev)
     return out, stats
 
 

@@ -29,7 +29,7 @@ def run(name, step, K=20):
     w = time.perf_counter()
     for _ in range(K):
         step()
-    b.record(pipe.compute_stream)
+    b.record(pipe.join())
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / K
     print(f"{name:40s} {ms:.4f} ms/step  wall {(time.perf_counter() - w) / K * 1e3:.4f}")

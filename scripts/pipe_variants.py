@@ -19,6 +19,6 @@ for name, inp, so in (("device", dev, None), ("host", host, None), ("host+stats"
     a.record(pipe.compute_stream); pipe.begin(a)
     for _ in range(20):
         pipe.submit(*inp, stats_out=so)
-    b.record(pipe.compute_stream)
+    b.record(pipe.join())
     torch.cuda.synchronize()
     print(name, round(a.elapsed_time(b) / 20, 4), "ms/step")

@@ -776,14 +776,62 @@ def test_pipeline_varying_batch_sizes_without_syncs():
         batches.append(pb)
         r = pipe.submit(pb.offsets, pb.channels, pb.xyz)
         # keep a device copy of each result, ordered after its batch
-        pipe.compute_stream.wait_event(r.ready)
-        with torch.cuda.stream(pipe.compute_stream):
-            results.append((r.grids.clone(), r.stats.clone()))
+        torch.cuda.current_stream().wait_event(r.ready)
+        results.append((r.grids.clone(), r.stats.clone()))
     torch.cuda.synchronize()
     for pb, (g, st) in zip(batches, results):
         g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
         assert_bitwise(g.cpu().numpy(), g_ref.cpu().numpy(), "varying sizes")
         assert np.array_equal(st.cpu().numpy(), s_ref.cpu().numpy())
+
+
+def test_pipeline_per_slot_compute_streams():
+    """Every slot runs its K3 on its own compute stream (the next batch's K3
+    starts in the previous one's tail). Same-size batches queued back to back,
+    each consumed on the caller's stream and released to the pipeline by an
+    event: every result equals the serial path. Submissions that rewrite the
+    same caller buffer stay ordered: the buffer ends with the last batch."""
+    from paper_2211_08506_b200.loader import GridPipeline
+
+    cfg = synth.CONFIGS[0]
+    spec = spec_of(cfg)
+    for depth in (2, 3):
+        pipe = GridPipeline(spec, depth=depth)
+        assert len(pipe.compute_streams) == depth
+        cur = torch.cuda.current_stream()
+        batches, results, released = [], [], []
+        for k in range(7):
+            pb = synth.packed_batch(cfg, range(100 * k, 100 * k + 48))
+            batches.append(pb)
+            rel = released[k - depth] if k >= depth else None   # consumer of the reused slot
+            r = pipe.submit(pb.offsets, pb.channels, pb.xyz, release=rel)
+            cur.wait_event(r.ready)
+            results.append((r.grids.clone(), r.stats.clone()))
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            released.append(ev)
+        done = torch.cuda.Event()
+        done.record(pipe.join())
+        done.synchronize()
+        torch.cuda.synchronize()
+        for pb, (g, st) in zip(batches, results):
+            g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+            assert_bitwise(g.cpu().numpy(), g_ref.cpu().numpy(), f"depth {depth}")
+            assert np.array_equal(st.cpu().numpy(), s_ref.cpu().numpy())
+    # the same caller buffer written by consecutive submissions (different
+    # compute streams): the writes stay in submission order
+    pipe = GridPipeline(spec, depth=2)
+    out = torch.empty((48, cfg.channels, *cfg.shape), dtype=torch.float32, device="cuda")
+    st = torch.empty((48, 2), dtype=torch.int64, device="cuda")
+    pipe.order_after(torch.cuda.current_stream())
+    last = None
+    for k in range(6):
+        pb = synth.packed_batch(cfg, range(100 * k, 100 * k + 48))
+        last = pipe.submit(pb.offsets, pb.channels, pb.xyz, out=out, stats=st)
+    last.ready.synchronize()
+    g_ref, s_ref = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+    assert_bitwise(out.cpu().numpy(), g_ref.cpu().numpy(), "same out, last batch")
+    assert np.array_equal(st.cpu().numpy(), s_ref.cpu().numpy())
 
 
 def test_pipeline_edge_batches():
