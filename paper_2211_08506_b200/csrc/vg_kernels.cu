@@ -512,6 +512,7 @@ struct SlabParams {
   int n_molecules;
   int gx_win;           // staged gx rows per candidate (window), 0: all CTA rows
   int gx_wmax;          // rows one warp spans in a row step (window padding)
+  int bulk;             // 1: stage tables with bulk copies (cp.async.bulk) where aligned
   // K2 candidate bins (NULL: scan the molecule's atoms)
   const int* bins;      // molecule b's bins start at bins + offsets[b] * n_jchunks
   const int* bin_off;   // [B][bin_nb + 1] offsets into the molecule's bins
@@ -534,6 +535,7 @@ struct BinParams {
 struct SlabShared {
   alignas(16) int warp_cnt[32];
   long long red[kMaxThreads / 32];
+  unsigned long long bar;   // row kernel: mbarrier of the bulk staging copies
 };
 
 __device__ __forceinline__ int lo16(int v) { return v & 0xffff; }
@@ -1175,6 +1177,39 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// mbarrier / bulk-copy primitives (bulk staging of vg_slab_kernel, and K3W)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "VG_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra VG_WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completing `bytes` of the
+// transaction count of mbarrier `bar`. Addresses 16-byte aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // First staged x row of a candidate under windowed gx staging: every warp
 // whose rows meet the x-support [xlo, xhi) reads rows within
 // [xlo - (wmax-1), xhi + wmax - 1); the window starts there (16-byte aligned
@@ -1228,6 +1263,59 @@ __device__ __forceinline__ void stage_tables(const SlabParams& p, const int4* me
     } else {
       for (int e = lane; e < zv1 - zv0; e += 32)
         cp_async4(dst + p.stage_gz + e, p.tz + a * p.rz + zv0 + e);
+    }
+  }
+}
+
+// The same staged blocks by 1-D bulk copies (cp.async.bulk, the TMA unit):
+// one thread per (candidate, table) pair issues one copy, so a CTA stages
+// ~85 candidates in a single pass of 3 warp instructions per warp, where
+// stage_tables issues three LDGSTS per candidate and warp behind the SM's
+// store queue. Completion is counted on `bar` (every warp arrives once with
+// its bytes as expect_tx): wait with mbar_wait(bar, parity) instead of
+// cp_async_wait_all() + __syncthreads(). Needs 16-byte aligned pieces: js % 4
+// == 0, row_base % 4 == 0, 4- or 8-voxel slots (the caller checks).
+template <int SW>
+__device__ __forceinline__ void stage_tables_bulk(const SlabParams& p, const int4* meta, int ns,
+                                                  unsigned stage_s, int js, int je, int row_base,
+                                                  int rows, int zv0, unsigned bar) {
+  const int lane = threadIdx.x & 31;
+  const unsigned gy_bytes = 4u * (unsigned)((je - js + 3) & ~3);
+  const unsigned gz_bytes = 4u * (unsigned)(p.zw * SW);
+  auto gx_piece = [&](const int4& m, int& g0) {   // bytes and first row of the gx piece
+    if (p.gx_win > 0) {
+      g0 = gx_window_start(p, m.x, row_base, true);
+      return 4u * (unsigned)(min(p.gx_win, p.rx - g0) & ~3);
+    }
+    g0 = row_base;
+    return 4u * (unsigned)((rows + 3) & ~3);
+  };
+  // this warp's bytes first (expect_tx precedes the copies), one arrival per warp
+  unsigned bytes = 0;
+  for (int e = (int)threadIdx.x; e < 3 * ns; e += (int)blockDim.x) {
+    const int q = e / 3, piece = e - 3 * q;
+    int g0;
+    bytes += piece == 0 ? gy_bytes : (piece == 2 ? gz_bytes : gx_piece(meta[q], g0));
+  }
+  const unsigned warp_bytes = __reduce_add_sync(kFull, bytes);
+  if (lane == 0) {
+    if (warp_bytes > 0) mbar_arrive_tx(bar, warp_bytes);
+    else mbar_arrive(bar);
+  }
+  __syncwarp();
+  for (int e = (int)threadIdx.x; e < 3 * ns; e += (int)blockDim.x) {
+    const int q = e / 3, piece = e - 3 * q;
+    const int4 m = meta[q];
+    const int64_t a = m.w;
+    const unsigned dst = stage_s + 4u * (unsigned)(q * p.stage_stride);
+    if (piece == 0) {
+      bulk_g2s(dst, p.ty + a * p.ry + js, gy_bytes, bar);
+    } else if (piece == 1) {
+      int g0;
+      const unsigned nb = gx_piece(m, g0);
+      if (nb > 0) bulk_g2s(dst + 4u * (unsigned)p.stage_gx, p.tx + a * p.rx + g0, nb, bar);
+    } else {
+      bulk_g2s(dst + 4u * (unsigned)p.stage_gz, p.tz + a * p.rz + zv0, gz_bytes, bar);
     }
   }
 }
@@ -1297,6 +1385,15 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   // Launched as a programmatic dependent of K1 (vg_generate_f32): wait until
   // K1 has completed and its tables are visible (a no-op otherwise).
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  const unsigned bar = smem_u32(&sh.bar);
+  unsigned bar_phase = 0;
+  if (p.bulk) {
+    if (tid == 0) {
+      mbar_init(bar, blockDim.x >> 5);   // one arrival per warp and staging round
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   RowTile T;
   // Linear CTA index. Channel-fused CTAs: the tiles of one molecule are
   // adjacent, so the CTAs staging the same atoms' tables run close together
@@ -1363,6 +1460,8 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   const unsigned gx_off = 4u * (unsigned)(p.stage_gx + T.r0);
   const int slot0 = ibase * p.D + zf;  // float offset in the slab
   const int rows = T.row_end - T.row_base;
+  // bulk staging needs 16-byte aligned pieces (x rows; y slabs checked per round)
+  const bool bulk_ok = p.bulk && SW >= 4 && (T.row_base & 3) == 0;
   const int rlo0 = T.row_base + T.wr0, rhi0 = T.row_base + T.wr1;
   const int64_t chan_elems = (int64_t)p.H * p.slab_elems;
 
@@ -1380,9 +1479,15 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
     int64_t pos = T.a0;
     const int n = build_list(p.supp, sh, meta_l, nullptr, pos, T.a1, fa);
     if (pos >= T.a1 && n <= p.stage_cap) {
-      stage_tables<SW>(p, meta_l, n, stage, j0, j1, T.row_base, rows, T.zv0, T.zv1);
-      cp_async_wait_all();
-      __syncthreads();
+      if (bulk_ok && (j0 & 3) == 0) {
+        stage_tables_bulk<SW>(p, meta_l, n, stage_s, j0, j1, T.row_base, rows, T.zv0, bar);
+        mbar_wait(bar, bar_phase);
+        bar_phase ^= 1u;
+      } else {
+        stage_tables<SW>(p, meta_l, n, stage, j0, j1, T.row_base, rows, T.zv0, T.zv1);
+        cp_async_wait_all();
+        __syncthreads();
+      }
       float* out_b = p.out + T.b * p.C * chan_elems + j0 * p.slab_elems + slot0;
       for (int c = 0; c < p.C; ++c) {
         Counts<M> cnt;
@@ -1445,12 +1550,21 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
         for (int s0 = 0; s0 < max(n, 1); s0 += p.stage_cap) {
           const int ns = min(p.stage_cap, n - s0);
           const int4* meta = meta_l + s0;
-          stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
+          const bool bulk = bulk_ok && (js & 3) == 0;   // uniform
+          if (bulk)
+            stage_tables_bulk<SW>(p, meta, ns, stage_s, js, je, T.row_base, rows, T.zv0, bar);
+          else
+            stage_tables<SW>(p, meta, ns, stage, js, je, T.row_base, rows, T.zv0, T.zv1);
           Counts<M> cnt;
           build_sublists<M>(p, meta, ns, -1, lists, stage_s, js, je, T.row_base, rlo0, rhi0, R, cnt);
           if (rounds == 0) VG_TS(9);
-          cp_async_wait_all();
-          __syncthreads();  // staged tables visible to every warp (lists are warp-private)
+          if (bulk) {
+            mbar_wait(bar, bar_phase);   // every warp's copies have landed
+            bar_phase ^= 1u;
+          } else {
+            cp_async_wait_all();
+            __syncthreads();  // staged tables visible to every warp (lists are warp-private)
+          }
           if (rounds == 0) VG_TS(2);
           ++rounds;
           staged += ns;
@@ -1529,38 +1643,6 @@ struct WsUnit {
   int gy_shift;  // js - (first staged gy slab): gy is staged from js & ~3
   int pad0, pad1;
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned a) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned a, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "VG_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra VG_WAIT_%=;\n}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine), completing `bytes` of the
-// transaction count of mbarrier `bar`. Addresses 16-byte aligned, bytes % 16 == 0.
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
 
 // Tile geometry shared by producer and consumers: lin -> (b, c, chunk, rblk, zblk)
 // in vg_slab_kernel's per-channel order (molecule fastest).
@@ -2780,6 +2862,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     }
   }
   if (env_int("VG_GXWIN", 1, 0, 1) == 0) p.gx_win = 0;
+  // bulk staging (cp.async.bulk + mbarrier): 16-byte table rows and z windows
+  p.bulk = sw >= 4 && (zw * sw) % 4 == 0 && env_int("VG_BULK", 1, 0, 1) == 1 ? 1 : 0;
   // Binned per-channel batches (large molecules): the persistent,
   // warp-specialised K3W when its alignment rules hold (8-voxel slots and
   // slab pairs, even y-chunks so every unit starts on an even slab, 16-byte
