@@ -2166,6 +2166,9 @@ __global__ void __launch_bounds__(kBinWarps * 32) vg_bin_kernel(const __grid_con
   int* start = bsm + kBinWarps * p.nb; // [nb]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = blockIdx.x;
+  // K3 directly follows on the stream (vg_slabs_f32 / vg_generate_f32): let its
+  // CTAs be scheduled now; they wait (griddepcontrol.wait) for this grid
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t a0 = __ldg(p.offsets + b), a1 = __ldg(p.offsets + b + 1);
   const int nb = p.nb, nch = p.nch;
   if (b == 0 && threadIdx.x == 0 && p.tile_counter != nullptr) *p.tile_counter = 0;
@@ -2826,6 +2829,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   const int z_blocks = P.z_blocks;
   const int64_t mean_atoms = P.mean_atoms;
   const bool fuse = P.fuse;
+  bool after_bins = false;   // K2 launched here, K3 directly behind it
   const int jc = P.jc;
   p.jc = jc;
   p.n_jchunks = P.n_jchunks;
@@ -2840,6 +2844,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     if (!bins_ready) {
       const int rc = launch_bins(d, L, ws, st, kernels);
       if (rc != VG_OK) return rc;
+      // K3 follows K2 on this stream: launched as its programmatic dependent
+      after_bins = env_int("VG_PDL", 1, 0, 1) == 1;
     }
   }
   p.row_blocks = row_blocks;
@@ -2935,6 +2941,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
   const dim3 grid((unsigned)ctas);
   int rc;
+  const bool pdl_saved = g_pdl_launch;
+  g_pdl_launch = g_pdl_launch || after_bins;
   if (sw == 8 && yp == 2)
     rc = launch_rows<8, 2>(M, grid, nt, smem, st, p);
   else if (sw == 8)
@@ -2943,6 +2951,7 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     rc = launch_rows<4, 1>(M, grid, nt, smem, st, p);
   else
     rc = launch_rows<1, 1>(M, grid, nt, smem, st, p);
+  g_pdl_launch = pdl_saved;
   if (rc != VG_OK) return rc;
   if (kernels != nullptr) *kernels += 1;
   return check_launch("vg_slab_kernel");
