@@ -77,6 +77,7 @@ constexpr int kTableThreads = 256;   // K1: 8 warps, one (atom, axis) each
 #define VG_LIST_CAP 128
 #endif
 constexpr int kListCap = VG_LIST_CAP;  // K3: candidate segment capacity (staged candidates max)
+constexpr int kFuseMeanAtoms = 64;   // K3: channel-fused CTAs up to this mean atom count
 constexpr int kC0CapMax = 1536;      // K3 row kernel: level-0 candidates kept per CTA (max)
 constexpr int kMaxCtaRows = 64;      // K3 row kernel: x rows per CTA (keeps staged rows short)
 constexpr int kMaxThreads = 512;     // K3: threads per CTA (upper bound)
@@ -1382,9 +1383,6 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   float* stage = reinterpret_cast<float*>(c0) + p.c0_cap;  // staged tables, then sublists
   const int tid = threadIdx.x, warp = tid >> 5;
 
-  // Launched as a programmatic dependent of K1 (vg_generate_f32): wait until
-  // K1 has completed and its tables are visible (a no-op otherwise).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const unsigned bar = smem_u32(&sh.bar);
   unsigned bar_phase = 0;
   if (p.bulk) {
@@ -1465,6 +1463,11 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   const int rlo0 = T.row_base + T.wr0, rhi0 = T.row_base + T.wr1;
   const int64_t chan_elems = (int64_t)p.H * p.slab_elems;
 
+  // Launched as a programmatic dependent of K1 / K2 (vg_generate_f32,
+  // vg_slabs_f32): wait until the preceding grid has completed and its supports,
+  // tables and bins are visible (a no-op otherwise). Everything above reads only
+  // launch parameters and the batch's offsets, so it overlaps that grid's tail.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   VG_TS(0);
   int nz = 0;
   int rounds = 0, staged = 0;
@@ -2610,7 +2613,7 @@ void plan_slabs(const vg_batch_desc& d, bool aligned16, SlabPlan* P) {
   // Channel fusion (one CTA serves all C channels of its tile from one staged
   // candidate list) for small molecules, whose whole atom list usually fits
   // the staging area; VG_FUSE=0/1 overrides (tuning hook).
-  bool fuse = d.C > 1 && mean_atoms <= kListCap / 2;
+  bool fuse = d.C > 1 && mean_atoms <= kFuseMeanAtoms;
   fuse = d.C > 1 && env_int("VG_FUSE", fuse ? 1 : 0, 0, 1) == 1;
   // Output bytes per CTA (measured on B200): fused CTAs ~1 MiB over all
   // channels; per-channel CTAs 256 KiB, halved for dense molecules (hundreds
@@ -2907,7 +2910,8 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   // reserved per CTA): the occupancy cliff costs more than extra halving.
   int cap_max = kListCap;
   cap_max = env_int("VG_CAP_MAX", cap_max, 1, kListCap);
-  const int want = (int)(mean_atoms * 2 < 32 ? 32 : (mean_atoms * 2 > cap_max ? cap_max : mean_atoms * 2));
+  const int64_t want_x = env_int("VG_WANT_X", 2, 1, 16);   // hook: capacity aim, x mean atoms
+  const int want = (int)(mean_atoms * want_x < 32 ? 32 : (mean_atoms * want_x > cap_max ? cap_max : mean_atoms * want_x));
   const int regs = (rows_regs(sw, yp, M) + 7) & ~7;   // allocation granularity
   const int reg_blocks = max(1, min(2048 / nt, 65536 / (regs * nt)));
   const int64_t per_cand = 4 * (int64_t)p.stage_stride + (int64_t)(nt / 32) * M * sizeof(int2);
