@@ -510,6 +510,11 @@ struct SlabParams {
   int fuse_channels;    // 1: one CTA serves every channel
   int cta_order;        // per-channel CTAs: 0 molecule fastest, 1 channel fastest
   int tasks;            // tiles per (molecule, channel): y-chunks x row-blocks x z-blocks
+  // tapered tail (channel-fused launches): CTAs from taper_lin on serve the
+  // molecules from taper_b on in y-chunks of jc2 slabs (tasks2 tiles each), so
+  // the launch ends on short CTAs and its SMs finish together
+  unsigned taper_lin;   // first tapered CTA (0xffffffff: none)
+  int taper_b, tasks2, jc2;
   int n_molecules;
   int gx_win;           // staged gx rows per candidate (window), 0: all CTA rows
   int gx_wmax;          // rows one warp spans in a row step (window padding)
@@ -1398,13 +1403,21 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   // while those are in L2. Per-channel CTAs (large molecules): molecule
   // fastest, which spreads the dense central tiles of a cluster over the
   // launch (measured better for cfg3).
-  int t, zblk = 0, rblk = 0;
+  int t, zblk = 0, rblk = 0, jc = p.jc;
   {
     const unsigned lin = blockIdx.x;
     if (p.fuse_channels) {
-      const unsigned b = lin / (unsigned)p.tasks;
-      t = (int)(lin - b * (unsigned)p.tasks);
-      T.b = b;
+      if (lin < p.taper_lin) {
+        const unsigned b = lin / (unsigned)p.tasks;
+        t = (int)(lin - b * (unsigned)p.tasks);
+        T.b = b;
+      } else {   // the launch's tail: shorter y-chunks
+        const unsigned l2 = lin - p.taper_lin;
+        const unsigned b = l2 / (unsigned)p.tasks2;
+        t = (int)(l2 - b * (unsigned)p.tasks2);
+        T.b = (unsigned)p.taper_b + b;
+        jc = p.jc2;
+      }
       T.c = 0;
     } else if (p.cta_order == 0) {
       const unsigned nb = (unsigned)p.n_molecules;
@@ -1434,8 +1447,8 @@ __global__ void __launch_bounds__(kRowThreads, row_minb(M)) vg_slab_kernel(const
   const int chunk = t;
   T.a0 = __ldg(p.offsets + T.b);
   T.a1 = __ldg(p.offsets + T.b + 1);
-  const int j0 = chunk * p.jc;
-  const int j1 = min(p.H, j0 + p.jc);
+  const int j0 = chunk * jc;
+  const int j1 = min(p.H, j0 + jc);
   const int zw = p.zw, R = p.rows_per_step;
   T.r0 = div_magic(tid, p.zw_magic);
   T.k = zblk * zw + (tid - T.r0 * zw);
@@ -2941,7 +2954,36 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
   p.cta_order = env_int("VG_ORDER", 0, 0, 1);
   p.tasks = p.n_jchunks * row_blocks * z_blocks;
   p.n_molecules = (int)d.n_molecules;
-  const int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
+  int64_t ctas = d.n_molecules * (fuse ? 1 : (int64_t)d.C) * p.tasks;
+  // Tapered tail (channel-fused launches of several waves): a launch ends when
+  // its last CTA does, and CTAs of ~1 MiB finish up to one CTA time (~40 us at
+  // cfg1) apart. The last molecules - about half a wave of full-size CTAs
+  // (VG_TAPER_Q quarter waves) - are cut into y-chunks a quarter as long
+  // (VG_TAPER_D; a multiple of 4 slabs, so their tables still stage by bulk
+  // copies): the SMs then finish within a short CTA's time of one another.
+  // Measured on B200: cfg1 K3 0.759 -> 0.751 ms, cfg4 1.4645 -> 1.4463; longer
+  // tails or other divisors are within 0.2%. Results do not depend on the tiling.
+  p.taper_lin = 0xffffffffu;
+  p.taper_b = 0;
+  p.tasks2 = p.tasks;
+  p.jc2 = jc;
+  const int taper = env_int("VG_TAPER", 1, 0, 2);   // hook: 0 off, 2 forced (a third of the batch)
+  if (fuse && taper > 0) {
+    const int64_t slots = (int64_t)sm_count() * blocks;
+    int jc2 = ((jc / env_int("VG_TAPER_D", 4, 2, 16) + 3) / 4) * 4;
+    if (jc2 < 4) jc2 = 4;
+    const int nch2 = (d.H + jc2 - 1) / jc2;
+    int64_t tail_mols = (env_int("VG_TAPER_Q", 2, 1, 16) * slots / 4 + p.tasks - 1) / p.tasks;
+    if (taper == 2) tail_mols = d.n_molecules / 3 > 0 ? d.n_molecules / 3 : 1;
+    if (jc2 * 2 <= jc && (ctas >= 4 * slots || taper == 2) && tail_mols < d.n_molecules) {
+      p.jc2 = jc2;
+      p.tasks2 = nch2 * row_blocks * z_blocks;
+      p.taper_b = (int)(d.n_molecules - tail_mols);
+      const int64_t head = (int64_t)p.taper_b * p.tasks;
+      ctas = head + tail_mols * p.tasks2;
+      if (head < 0xffffffffll) p.taper_lin = (unsigned)head;
+    }
+  }
   if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
   const dim3 grid((unsigned)ctas);
   int rc;

@@ -561,6 +561,23 @@ def test_slab_pair_hot_loop_variants(monkeypatch, yp):
     _compare_with_oracle(synth.CONFIGS[0], range(64))
 
 
+@pytest.mark.parametrize("env", [{"VG_TAPER": "2", "VG_TASK_KB": "1024"},
+                                 {"VG_TAPER": "2", "VG_TASK_KB": "1024", "VG_BULK": "0"},
+                                 {"VG_TAPER": "0"}, {"VG_BULK": "0"}])
+def test_tapered_tail_and_staging_variants_vs_oracle(env, monkeypatch):
+    """The launch's tapered tail (the last molecules in quarter-length
+    y-chunks; VG_TAPER=2 forces it on small batches, a third of the molecules,
+    VG_TASK_KB keeps the full-size tiles the taper divides)
+    and both staging paths (bulk copies / cp.async: VG_BULK) are bit-exact vs
+    the oracle on fused batches, incl. large molecules that fall back to
+    per-channel passes, with identical counters."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _compare_with_oracle(synth.CONFIGS[1], range(0, 1024, 17))
+    _compare_with_oracle(synth.CONFIGS[0], range(64))
+    _compare_with_oracle(synth.CONFIGS[4], range(0, 4096, 29))
+
+
 def test_fused_cta_fallback_on_large_molecules_vs_oracle(monkeypatch):
     """Channel-fused CTAs on molecules too large for one staging pass fall
     back to the per-channel path (halved sub-chunks, segmented slabs);
