@@ -215,3 +215,28 @@ def test_launches_follow_the_output_device():
         res.ready.synchronize()
     assert_bitwise(g.cpu().numpy(), ref.cpu().numpy(), "cuda:1")
     assert_bitwise(res.grids.cpu().numpy(), ref.cpu().numpy(), "pipeline cuda:1")
+
+
+def test_bench_gpus2_runs_two_ranks_with_kernels():
+    """`bench.py --gpus 2` with kernels: the script spawns two ranks (sharing
+    cuda:0 on a one-GPU box: gloo carries the barrier and the max over ranks),
+    each generates its half of the batch, and rank 0 prints one line with the
+    whole job's rate, the contract's keys and both ranks' shares."""
+    import json
+    import os
+
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    res = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--config", "0",
+                          "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["global_batch"] == 64
+    assert [r["molecules"] for r in line["per_rank"]] == [32, 32] or \
+        sum(r["molecules"] for r in line["per_rank"]) == 64
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    for key in ("roofline", "clocks", "ms_per_step", "higher_is_better"):
+        assert key in line
