@@ -1,6 +1,6 @@
 # Interleaved A/B of library builds (R rounds, median per build and config):
 # R=3 CFGS="3 4" bash scripts/gpu_abr.sh libA.so libB.so [ENVSPEC...]
-# A build may carry env settings: "libvoxgrid_b200.so:VG_ROT=0"
+# A build may carry env settings: "libvoxgrid_b200.so:VG_BULK=0"
 mkdir -p gpurun_out
 rm -f gpurun_out/abr.txt
 for r in $(seq ${R:-3}); do
