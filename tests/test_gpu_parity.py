@@ -620,6 +620,42 @@ def test_estimator_packed_fast_path_equals_per_sample_path():
         est.transform(bad)
 
 
+def test_transform_back_to_back_calls_recycle_outputs_safely():
+    """Consecutive transform calls whose outputs are consumed on the caller's
+    stream or a side stream (a device-side digest, then dropped, no host sync):
+    the caching allocator recycles the outputs across calls while the pipeline's
+    compute streams write them, and every digest still equals the serial path's."""
+    cfg = synth.CONFIGS[0]
+    spec = spec_of(cfg)
+    est = None
+    want, got = [], []
+    side = torch.cuda.Stream()
+    for k in range(14):
+        n = (48, 48, 17, 48, 64, 48)[k % 6]
+        pb = synth.packed_batch(cfg, range(70 * k, 70 * k + n))
+        X = [np.column_stack([pb.channels[a:b].astype(np.float64), pb.xyz.reshape(-1, 3)[a:b]])
+             for a, b in zip(pb.offsets[:-1], pb.offsets[1:])]
+        if est is None:
+            est = vg.GaussianVoxelizer(grid_size=cfg.shape, sigma=cfg.sigma,
+                                       n_channels=cfg.channels,
+                                       box=(cfg.box_origin, cfg.box_extents)).fit(X)
+        g = est.transform(X)
+        if k % 3 == 2:   # a consumer on another stream, ordered after the caller's
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                got.append(g.view(torch.int32).sum(dim=(1, 2, 3, 4), dtype=torch.int64))
+            g.record_stream(side)
+        else:
+            got.append(g.view(torch.int32).sum(dim=(1, 2, 3, 4), dtype=torch.int64))
+        del g
+        ref, _ = vg.generate_packed(pb.offsets, pb.channels, pb.xyz, spec)
+        want.append(ref.view(torch.int32).sum(dim=(1, 2, 3, 4), dtype=torch.int64))
+        del ref
+    torch.cuda.synchronize()
+    for k, (a, b) in enumerate(zip(got, want)):
+        assert torch.equal(a.cpu(), b.cpu()), k
+
+
 def test_transform_chunked_pipeline_equals_single_launch():
     """transform's chunked, pipelined path (loader.generate_rows: pinned
     staging, one GridPipeline submit per chunk into slices of one output)
