@@ -64,7 +64,8 @@ typedef struct vg_mol_stats {
   int64_t nonzero_voxels;
 } vg_mol_stats;
 
-/* Byte offsets of the per-atom tables inside the workspace (all 256-aligned).
+/* Byte offsets of the per-atom tables inside the workspace (all 256-aligned;
+ * the workspace pointer itself must be 16-byte aligned: VG_ERR_INVALID otherwise).
  * tx: [n_atoms][row_x] fp32 masses along x (W used), ty: [n_atoms][row_y] (H),
  * tz: [n_atoms][row_z] (D); supp: [n_atoms] x int32[4] =
  * {xlo | xhi<<16, ylo | yhi<<16, zlo | zhi<<16, channel} (AxisTable.support,

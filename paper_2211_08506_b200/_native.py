@@ -29,6 +29,7 @@ NVCC_FLAGS = [
 ]
 
 VG_OK = 0
+VG_ERR_INVALID = -1
 VG_ERR_WORKSPACE = -3
 
 

@@ -3016,6 +3016,9 @@ int prepare(const vg_batch_desc* desc, float* out, void* workspace, size_t works
   if (workspace == nullptr || workspace_bytes < L->total)
     return set_error(VG_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L->total,
                      workspace_bytes);
+  // the table rows are staged with 16-byte copies (cp.async / cp.async.bulk)
+  if (reinterpret_cast<uintptr_t>(workspace) % 16 != 0)
+    return set_error(VG_ERR_INVALID, "workspace must be 16-byte aligned");
   return VG_OK;
 }
 

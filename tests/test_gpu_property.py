@@ -138,3 +138,8 @@ def test_workspace_and_stats_stay_in_bounds(k):
     assert_bitwise(out.cpu().numpy(), ref, f"guarded cfg{k}")
     st = stbuf[128:134].view(3, 2).cpu().numpy()
     assert [int(v) for v in st[:, 1]] == [r["nonzero_voxels"] for r in rs]
+    # a workspace that is not 16-byte aligned is refused (the table rows are
+    # staged with 16-byte copies), before anything is launched
+    rc = lib.vg_generate_f32(desc, out.data_ptr(), ws_ptr + 4, layout.total, st_ptr,
+                             torch.cuda.current_stream().cuda_stream)
+    assert rc == _native.VG_ERR_INVALID and b"16-byte" in lib.vg_last_error()
