@@ -724,6 +724,9 @@ def run_b200(args):
                 "atoms_rank0": n_atoms,
                 "parallelism": f"molecule-sharded x{world} (cost-balanced contiguous ranges), "
                                f"no collective; timing plumbing over {backend}",
+                "pipeline": f"GridPipeline depth {len(pipe.slots)}, {len(pipe.compute_streams)} "
+                            "compute streams (one per slot: consecutive K3s overlap their tails); "
+                            "value_serial runs K1 then K3 on one stream",
                 "l2": (f"flushed: each step writes {alg_bytes / 1e6:.0f} MB, which fits the "
                        f"{l2_bytes >> 20} MB L2, so a {4 * l2_bytes >> 20} MB store stream runs "
                        "before every timed step (not timed); value and e2e are then per-step "
