@@ -2988,6 +2988,13 @@ int launch_slabs(const vg_batch_desc& d, const vg_ws_layout& L, char* ws, float*
     }
   }
   if (ctas > INT_MAX) return set_error(VG_ERR_INVALID, "too many CTAs (%lld)", (long long)ctas);
+  if (env_int("VG_DEBUG_PLAN", 0, 0, 1) == 1)   // test hook: the launch plan on stderr
+    fprintf(stderr,
+            "[vg plan] nt=%d M=%d R=%d rb=%d zb=%d jc=%d chunks=%d fuse=%d cap=%d bulk=%d ctas=%lld "
+            "taper_b=%d jc2=%d tasks2=%d bins=%d\n",
+            nt, M, R, row_blocks, z_blocks, jc, p.n_jchunks, (int)fuse, p.stage_cap, p.bulk,
+            (long long)ctas, p.taper_lin == 0xffffffffu ? -1 : p.taper_b, p.jc2, p.tasks2,
+            p.bins != nullptr);
   const dim3 grid((unsigned)ctas);
   int rc;
   const bool pdl_saved = g_pdl_launch;

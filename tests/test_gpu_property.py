@@ -1,4 +1,4 @@
-"""Randomised parity (hypothesis, 1000 + 300 derandomised cases): random shapes, channel counts, boxes,
+"""Randomised parity (hypothesis, 1000 + 250 + 300 derandomised cases): random shapes, channel counts, boxes,
 sigmas, thresholds, periodic cells and molecule sizes, GPU path vs the CPU
 oracle, bit for bit, with identical GenStats counters. Complements the fixed
 cases of test_gpu_parity.py with inputs nobody chose by hand. The outputs sit
@@ -69,6 +69,67 @@ def test_random_batches_match_oracle(case):
     geom = orc.Geometry((H, W, D), C, origin, ext, sigma, periodic)
     ref, rs = orc.batch(offsets, ch, xyz, geom, threshold=thr)
     assert_bitwise(grids.cpu().numpy(), ref, f"random case {case}")
+    st_h = st_.cpu().numpy()
+    assert [int(v) for v in st_h[:, 0]] == [r["voxel_writes"] for r in rs]
+    assert [int(v) for v in st_h[:, 1]] == [r["nonzero_voxels"] for r in rs]
+
+
+@st.composite
+def fused_batches(draw):
+    H = draw(st.integers(8, 40))
+    W = draw(st.integers(1, 40))
+    D = draw(st.sampled_from([4, 8, 12, 16, 20, 24, 32, 40, 7, 13]))
+    C = draw(st.integers(2, 6))
+    ext = tuple(draw(st.floats(2.0, 12.0)) for _ in range(3))
+    sigma = draw(st.floats(0.1, 1.0))
+    thr = draw(st.one_of(st.none(), st.floats(1e-7, 0.05)))
+    sizes = draw(st.lists(st.integers(0, 90), min_size=4, max_size=14))
+    seed = draw(st.integers(0, 2**31 - 1))
+    bulk = draw(st.booleans())
+    return H, W, D, C, ext, sigma, thr, sizes, seed, bulk
+
+
+@settings(max_examples=250, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(fused_batches())
+def test_random_fused_batches_with_tapered_tail_match_oracle(case):
+    """The two-kernel path (VG_SMALL=0) with the launch's tapered tail forced
+    (VG_TAPER=2: the last third of the molecules in quarter-length y-chunks;
+    VG_TASK_KB keeps long chunks to divide) on random shapes, with bulk-copy or
+    cp.async staging: bit-exact vs the oracle, counters identical, nothing
+    written outside the grids."""
+    import os
+
+    H, W, D, C, ext, sigma, thr, sizes, seed, bulk = case
+    origin = (0.0, 0.0, 0.0)
+    rng = np.random.default_rng(seed)
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(offsets[-1])
+    xyz = rng.uniform(-1.0, np.array(ext) + 1.0, (n, 3))
+    ch = rng.integers(0, C, n).astype(np.int32)
+    spec = vg.GridSpec((H, W, D), C, vg.BoundingBox(origin, ext), sigma)
+    B = len(sizes)
+    n_out = B * C * H * W * D
+    guard = 4096
+    buf = torch.full((guard + n_out + guard,), -7.0, device="cuda")
+    grids = buf[guard:guard + n_out].view(B, C, H, W, D)
+    hooks = {"VG_SMALL": "0", "VG_TAPER": "2", "VG_TASK_KB": "4096", "VG_FUSE": "1",
+             "VG_BULK": "1" if bulk else "0"}
+    old = {k: os.environ.get(k) for k in hooks}
+    os.environ.update(hooks)
+    try:
+        _, st_ = vg.generate_packed(offsets, ch, xyz, spec, threshold=thr, out=grids)
+        torch.cuda.synchronize()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert bool((buf[:guard] == -7.0).all()) and bool((buf[guard + n_out:] == -7.0).all())
+    geom = orc.Geometry((H, W, D), C, origin, ext, sigma, False)
+    ref, rs = orc.batch(offsets, ch, xyz, geom, threshold=thr)
+    assert_bitwise(grids.cpu().numpy(), ref, f"tapered case {case}")
     st_h = st_.cpu().numpy()
     assert [int(v) for v in st_h[:, 0]] == [r["voxel_writes"] for r in rs]
     assert [int(v) for v in st_h[:, 1]] == [r["nonzero_voxels"] for r in rs]
