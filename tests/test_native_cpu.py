@@ -237,3 +237,15 @@ def test_accumulation_is_never_contracted_to_fma(lib):
     for name, body in funcs.items():
         if "vg_small_kernel" in name:
             assert "FFMA2" not in "\n".join(body), name
+
+
+def test_slab_kernel_stages_with_bulk_copies_and_streaming_stores(lib):
+    """The shipped K3 instances carry what DESIGN.md §5 describes: bulk-copy
+    staging (UBLKCP) awaited on an mbarrier (SYNCS ... TRYWAIT), the cp.async
+    path for unaligned rounds (LDGSTS) and 128-bit evict-first stores."""
+    funcs = _sass_by_function()
+    k3 = {n: "\n".join(b) for n, b in funcs.items() if "vg_slab_kernelILi1ELi8ELi2E" in n}
+    assert len(k3) == 1, sorted(funcs)[:5]
+    text = next(iter(k3.values()))
+    for needle in ("UBLKCP", "SYNCS.ARRIVE", "TRYWAIT", "LDGSTS", "STG.E.EF.128"):
+        assert needle in text, needle
